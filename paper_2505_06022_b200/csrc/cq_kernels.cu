@@ -1,0 +1,582 @@
+// libcq compute kernels for sm_100a.
+//
+// These replace the reference's per-cell Python evaluation
+// (pkg/src/clusterq/simulator.py:151-158 -> kernel.py:291-331 eval_kernel,
+// model.py:442-453 ReadView.read).  Arithmetic is performed with one
+// rounding per DSL operator in the DSL's left-to-right tree order (no FMA
+// contraction: explicit __*_rn intrinsics), so float64 results are
+// bit-identical to the reference and float32 results are bit-identical to a
+// binary32 restatement of the same tree.
+#include <cstring>
+#include <type_traits>
+
+#include "cq_common.cuh"
+
+namespace cq {
+
+// ------------------------------------------------------------ arithmetic
+template <typename T> struct Ar;
+template <> struct Ar<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b, bool&) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double neg(double a) { return -a; }
+  static __device__ __forceinline__ double from_id(int64_t i) { return (double)i; }
+  static __device__ __forceinline__ double from_bits(int64_t b) { return __longlong_as_double(b); }
+};
+template <> struct Ar<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b, bool&) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float neg(float a) { return -a; }
+  static __device__ __forceinline__ float from_id(int64_t i) { return __ll2float_rn(i); }
+  // constants arrive as binary64 bit patterns; round once to binary32
+  static __device__ __forceinline__ float from_bits(int64_t b) { return __double2float_rn(__longlong_as_double(b)); }
+};
+// wrapping two's-complement int64, truncating division (kernel.py:275-288, 315-321)
+template <> struct Ar<long long> {
+  typedef unsigned long long U;
+  static __device__ __forceinline__ long long add(long long a, long long b) { return (long long)((U)a + (U)b); }
+  static __device__ __forceinline__ long long sub(long long a, long long b) { return (long long)((U)a - (U)b); }
+  static __device__ __forceinline__ long long mul(long long a, long long b) { return (long long)((U)a * (U)b); }
+  static __device__ __forceinline__ long long div(long long a, long long b, bool& fail) {
+    if (b == 0) { fail = true; return 0; }
+    U ua = a < 0 ? (U)0 - (U)a : (U)a;
+    U ub = b < 0 ? (U)0 - (U)b : (U)b;
+    U q = ua / ub;
+    return (long long)(((a < 0) != (b < 0)) ? (U)0 - q : q);
+  }
+  static __device__ __forceinline__ long long neg(long long a) { return (long long)((U)0 - (U)a); }
+  static __device__ __forceinline__ long long from_id(int64_t i) { return (long long)i; }
+  static __device__ __forceinline__ long long from_bits(int64_t b) { return (long long)b; }
+};
+
+__device__ __forceinline__ int64_t view_off(const cq_view_t& v, int64_t p0, int64_t p1, int64_t p2) {
+  return (p0 - v.alloc.lo[0]) * v.stride[0] + (p1 - v.alloc.lo[1]) * v.stride[1] +
+         (p2 - v.alloc.lo[2]) * v.stride[2];
+}
+
+__device__ __forceinline__ int64_t clamp64(int64_t v, int64_t lo, int64_t hi_excl) {
+  return v < lo ? lo : (v >= hi_excl ? hi_excl - 1 : v);
+}
+
+static inline int64_t box_volume(const cq_box_t& b) {
+  int64_t v = 1;
+  for (int k = 0; k < CQ_MAX_DIMS; ++k) v *= (b.hi[k] - b.lo[k]);
+  return v;
+}
+
+static inline int grid_for(int64_t work, int threads, int sm_count, int per_sm) {
+  int64_t g = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count * per_sm;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// First-error record: key = (row-major cell index << 4) | code, atomicMin.
+__device__ void report_error(unsigned long long* flag, int code, int64_t lin, int64_t p0, int64_t p1,
+                             int64_t p2) {
+  unsigned long long key = ((unsigned long long)lin << 4) | (unsigned long long)code;
+  unsigned long long old = atomicMin(flag, key);
+  if (old > key) {
+    long long* pt = (long long*)(flag + 1);
+    pt[0] = p0;
+    pt[1] = p1;
+    pt[2] = p2;
+  }
+}
+
+// ------------------------------------------------------------------- fill
+template <typename T>
+__global__ void fill_kernel(cq_view_t dst, cq_box_t box, cq_box_t extent, int mode, T value) {
+  int64_t n1 = box.hi[1] - box.lo[1], n2 = box.hi[2] - box.lo[2];
+  int64_t total = (box.hi[0] - box.lo[0]) * n1 * n2;
+  int64_t e1 = extent.hi[1] - extent.lo[1], e2 = extent.hi[2] - extent.lo[2];
+  T* out = (T*)dst.ptr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i2 = t % n2, r = t / n2;
+    int64_t i1 = r % n1, i0 = r / n1;
+    int64_t p0 = box.lo[0] + i0, p1 = box.lo[1] + i1, p2 = box.lo[2] + i2;
+    T v;
+    if (mode == 1) v = Ar<T>::from_id((p0 * e1 + p1) * e2 + p2);
+    else v = value;
+    out[view_off(dst, p0, p1, p2)] = v;
+  }
+}
+
+// ------------------------------------------------------------------ SAXPY
+// 16-byte vector loads/stores, grid-stride; one rounding per operator.
+template <typename T>
+__global__ void __launch_bounds__(256) saxpy_kernel(T alpha, const T* __restrict__ x,
+                                                    const T* __restrict__ y, T* __restrict__ z,
+                                                    int64_t n) {
+  constexpr int V = 16 / sizeof(T);
+  typedef typename std::conditional<sizeof(T) == 4, float4, double2>::type Vec;
+  int64_t nv = n / V;
+  const Vec* xv = reinterpret_cast<const Vec*>(x);
+  const Vec* yv = reinterpret_cast<const Vec*>(y);
+  Vec* zv = reinterpret_cast<Vec*>(z);
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // two independent vectors in flight per thread
+  for (; t + stride < nv; t += 2 * stride) {
+    Vec a0 = __ldcs(xv + t), b0 = __ldcs(yv + t);
+    Vec a1 = __ldcs(xv + t + stride), b1 = __ldcs(yv + t + stride);
+    T* pa0 = reinterpret_cast<T*>(&a0);
+    T* pb0 = reinterpret_cast<T*>(&b0);
+    T* pa1 = reinterpret_cast<T*>(&a1);
+    T* pb1 = reinterpret_cast<T*>(&b1);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      pa0[k] = Ar<T>::add(Ar<T>::mul(alpha, pa0[k]), pb0[k]);
+      pa1[k] = Ar<T>::add(Ar<T>::mul(alpha, pa1[k]), pb1[k]);
+    }
+    __stcs(zv + t, a0);
+    __stcs(zv + t + stride, a1);
+  }
+  for (; t < nv; t += stride) {
+    Vec a0 = __ldcs(xv + t), b0 = __ldcs(yv + t);
+    T* pa0 = reinterpret_cast<T*>(&a0);
+    T* pb0 = reinterpret_cast<T*>(&b0);
+#pragma unroll
+    for (int k = 0; k < V; ++k) pa0[k] = Ar<T>::add(Ar<T>::mul(alpha, pa0[k]), pb0[k]);
+    __stcs(zv + t, a0);
+  }
+  int64_t tail = nv * V + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tail < n) z[tail] = Ar<T>::add(Ar<T>::mul(alpha, x[tail]), y[tail]);
+}
+
+__global__ void saxpy_i64_kernel(long long alpha, const long long* x, const long long* y, long long* z,
+                                 int64_t n) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    z[t] = Ar<long long>::add(Ar<long long>::mul(alpha, x[t]), y[t]);
+}
+
+// ---------------------------------------------------------------- wave 5pt
+// out = ((k2*u) - upr) + (c*((((uN + uS) + uW) + uE) - (k4*u)))   [DSL tree]
+template <typename T>
+__device__ __forceinline__ T wave_cell(T u, T upr, T n, T s, T w, T e, T c, T k2, T k4) {
+  typedef Ar<T> A;
+  T lap = A::sub(A::add(A::add(A::add(n, s), w), e), A::mul(k4, u));
+  return A::add(A::sub(A::mul(k2, u), upr), A::mul(c, lap));
+}
+
+// Vectorised row-marching kernel.  A thread owns V consecutive columns and
+// walks RB rows downwards keeping rows r-1, r, r+1 of u in registers, so u is
+// read from DRAM once per cell (12 B/cell/step for f32: u, upr, out).  West/
+// east neighbours come from adjacent lanes by shuffle; warp-edge lanes fetch
+// one extra scalar (an L1 hit).  Requirements (host-checked): the box spans
+// whole rows [0, W) of the innermost axis, W % V == 0, views 16-B aligned
+// with row pitch % V == 0.
+template <typename T, int RB>
+__global__ void __launch_bounds__(256) wave5_rows_kernel(cq_view_t u, cq_view_t upr, cq_view_t out,
+                                                         int64_t row_lo, int64_t row_hi, int64_t H,
+                                                         int64_t W, T c, T k2, T k4) {
+  constexpr int V = 16 / sizeof(T);
+  typedef typename std::conditional<sizeof(T) == 4, float4, double2>::type Vec;
+  const int lane = threadIdx.x & 31;
+  const int64_t col = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
+  const int64_t r0 = row_lo + (int64_t)blockIdx.y * RB;
+  if (r0 >= row_hi) return;
+  const int64_t r1 = min(r0 + (int64_t)RB, row_hi);
+  const bool active = col < W;
+  const int64_t cc = active ? col : 0;
+  const T* ub = (const T*)u.ptr;
+  const T* pb = (const T*)upr.ptr;
+  T* ob = (T*)out.ptr;
+  const int64_t us = u.stride[1], ps = upr.stride[1], os = out.stride[1];
+  // rows live on axis 1, columns on axis 2 (leading axis 0 is [0,1))
+  auto urow = [&](int64_t r) -> const T* {
+    r = clamp64(r, 0, H);
+    return ub + (r - u.alloc.lo[1]) * us + (cc - u.alloc.lo[2]);
+  };
+  Vec vm = *reinterpret_cast<const Vec*>(urow(r0 - 1));
+  Vec vc = *reinterpret_cast<const Vec*>(urow(r0));
+  const bool west_edge = (lane == 0);
+  const bool east_edge = (lane == 31) || (col + V >= W);
+  for (int64_t r = r0; r < r1; ++r) {
+    Vec vn = *reinterpret_cast<const Vec*>(urow(r + 1));
+    const T* prow = pb + (r - upr.alloc.lo[1]) * ps + (cc - upr.alloc.lo[2]);
+    Vec vp = *reinterpret_cast<const Vec*>(prow);
+    const T* cur = reinterpret_cast<const T*>(&vc);
+    const T* up_ = reinterpret_cast<const T*>(&vm);
+    const T* dn = reinterpret_cast<const T*>(&vn);
+    const T* pr = reinterpret_cast<const T*>(&vp);
+    // west neighbour of element 0, east neighbour of element V-1
+    T wnb = __shfl_up_sync(0xffffffffu, cur[V - 1], 1);
+    T enb = __shfl_down_sync(0xffffffffu, cur[0], 1);
+    const T* crow = urow(r);
+    if (west_edge) wnb = (cc == 0) ? cur[0] : crow[-1];
+    if (east_edge) enb = (cc + V >= W) ? cur[V - 1] : crow[V];
+    Vec vo;
+    T* o = reinterpret_cast<T*>(&vo);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      T w = (k == 0) ? wnb : cur[k - 1];
+      T e = (k == V - 1) ? enb : cur[k + 1];
+      o[k] = wave_cell<T>(cur[k], pr[k], up_[k], dn[k], w, e, c, k2, k4);
+    }
+    if (active) *reinterpret_cast<Vec*>(ob + (r - out.alloc.lo[1]) * os + (cc - out.alloc.lo[2])) = vo;
+    vm = vc;
+    vc = vn;
+  }
+}
+
+// Generic per-cell fallback for any box / alignment.
+template <typename T>
+__global__ void wave5_cell_kernel(cq_view_t u, cq_view_t upr, cq_view_t out, cq_box_t box,
+                                  int64_t H, int64_t W, T c, T k2, T k4) {
+  int64_t n1 = box.hi[1] - box.lo[1], n2 = box.hi[2] - box.lo[2];
+  int64_t total = (box.hi[0] - box.lo[0]) * n1 * n2;
+  const T* ub = (const T*)u.ptr;
+  const T* pb = (const T*)upr.ptr;
+  T* ob = (T*)out.ptr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j = box.lo[2] + t % n2, r = t / n2;
+    int64_t i = box.lo[1] + r % n1, p0 = box.lo[0] + r / n1;
+    int64_t im = clamp64(i - 1, 0, H), ip = clamp64(i + 1, 0, H);
+    int64_t jm = clamp64(j - 1, 0, W), jp = clamp64(j + 1, 0, W);
+    T uc = ub[view_off(u, p0, i, j)];
+    T v = wave_cell<T>(uc, pb[view_off(upr, p0, i, j)], ub[view_off(u, p0, im, j)],
+                       ub[view_off(u, p0, ip, j)], ub[view_off(u, p0, i, jm)],
+                       ub[view_off(u, p0, i, jp)], c, k2, k4);
+    ob[view_off(out, p0, i, j)] = v;
+  }
+}
+
+// ------------------------------------------------------- expression kernel
+template <typename T>
+__device__ __forceinline__ T load_as(const cq_view_t& v, int kind, int64_t off) {
+  if (kind == CQ_F64) return (T)((const double*)v.ptr)[off];
+  if (kind == CQ_F32) return (T)((const float*)v.ptr)[off];
+  return (T)((const long long*)v.ptr)[off];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) expr_kernel(const __grid_constant__ cq_expr_t X,
+                                                   unsigned long long* flag) {
+  int64_t n1 = X.box.hi[1] - X.box.lo[1], n2 = X.box.hi[2] - X.box.lo[2];
+  int64_t total = (X.box.hi[0] - X.box.lo[0]) * n1 * n2;
+  const int kdims = X.dims;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p[3];
+    p[2] = X.box.lo[2] + t % n2;
+    int64_t r = t / n2;
+    p[1] = X.box.lo[1] + r % n1;
+    p[0] = X.box.lo[0] + r / n1;
+    T results[CQ_EXPR_MAX_OUT];
+    bool failed = false;
+    for (int o = 0; o < X.n_out; ++o) {
+      T stack[32];
+      int sp = 0;
+      for (int pc = X.out_code_begin[o]; pc < X.out_code_end[o]; ++pc) {
+        int op = X.code_op[pc], arg = X.code_arg[pc];
+        switch (op) {
+          case 0: stack[sp++] = Ar<T>::from_bits(X.consts[arg]); break;
+          case 1: stack[sp++] = Ar<T>::from_id(p[arg]); break;
+          case 2: {
+            int vi = X.slot_view[arg];
+            const cq_view_t& v = X.views[vi];
+            int bd = X.view_dims[vi];
+            int64_t q[3] = {0, 0, 0};
+            for (int j = 0; j < bd; ++j) {
+              int64_t x = p[3 - kdims + j] + X.slot_off[arg][j];
+              int ax = 3 - bd + j;
+              q[ax] = clamp64(x, X.view_extent[vi].lo[ax], X.view_extent[vi].hi[ax]);
+            }
+            int nchk = X.view_n_check[vi];
+            if (nchk > 0) {
+              bool inside = false;
+              for (int b = 0; b < nchk && !inside; ++b) {
+                const cq_box_t& cb = X.view_check[vi][b];
+                inside = q[0] >= cb.lo[0] && q[0] < cb.hi[0] && q[1] >= cb.lo[1] && q[1] < cb.hi[1] &&
+                         q[2] >= cb.lo[2] && q[2] < cb.hi[2];
+              }
+              if (!inside) {
+                report_error(flag, CQ_ERR_MAPPER, t, p[0], p[1], p[2]);
+                failed = true;
+                stack[sp++] = (T)0;
+                break;
+              }
+            }
+            stack[sp++] = load_as<T>(v, X.kind, view_off(v, q[0], q[1], q[2]));
+            break;
+          }
+          case 3: stack[sp - 1] = Ar<T>::neg(stack[sp - 1]); break;
+          default: {
+            T b = stack[--sp];
+            T a = stack[sp - 1];
+            T res;
+            if (op == 4) res = Ar<T>::add(a, b);
+            else if (op == 5) res = Ar<T>::sub(a, b);
+            else if (op == 6) res = Ar<T>::mul(a, b);
+            else {
+              bool dz = false;
+              res = Ar<T>::div(a, b, dz);
+              if (dz) {
+                report_error(flag, CQ_ERR_EVAL, t, p[0], p[1], p[2]);
+                failed = true;
+              }
+            }
+            stack[sp - 1] = res;
+          }
+        }
+      }
+      results[o] = stack[0];
+    }
+    if (failed) continue;
+    for (int o = 0; o < X.n_out; ++o) {
+      const cq_view_t& v = X.out[o];
+      int64_t off = view_off(v, p[0], p[1], p[2]);
+      if (X.kind == CQ_F64) ((double*)v.ptr)[off] = (double)results[o];
+      else if (X.kind == CQ_F32) ((float*)v.ptr)[off] = (float)results[o];
+      else ((long long*)v.ptr)[off] = (long long)results[o];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ N-body
+// Block = 8 warps x 32 lanes; a lane owns NB_IPT i-bodies, so a block covers
+// 32*NB_IPT i-bodies and its 8 warps split the j range into 8 fixed slices
+// of [0, n) (independent of the i partition, so results are bit-identical
+// for any GPU count).  Each warp stages 32 j-bodies per tile in shared
+// memory and every lane reads them back by broadcast (LDS.128); partial
+// accelerations are summed over the warps in fixed order.
+constexpr int NB_WARPS = 8;
+constexpr int NB_IPT = 2;
+constexpr int NB_IBLOCK = 32 * NB_IPT;
+
+__device__ __forceinline__ void nb_interact(const float4& pi, const float4& pj, float eps2, float& ax,
+                                            float& ay, float& az) {
+  float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+  float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
+  float inv = rsqrtf(r2);
+  float s = pj.w * (inv * inv * inv);
+  ax = fmaf(dx, s, ax);
+  ay = fmaf(dy, s, ay);
+  az = fmaf(dz, s, az);
+}
+
+__global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4* __restrict__ pos,
+                                                                   int64_t n, const float4* vel_in,
+                                                                   float4* vel, int64_t i_lo,
+                                                                   int64_t i_hi, float eps2, float dt) {
+  __shared__ float4 tile[NB_WARPS][32];
+  __shared__ float part[NB_WARPS][3][NB_IBLOCK];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ibase = i_lo + (int64_t)blockIdx.x * NB_IBLOCK;
+  float4 pi[NB_IPT];
+  float ax[NB_IPT], ay[NB_IPT], az[NB_IPT];
+#pragma unroll
+  for (int q = 0; q < NB_IPT; ++q) {
+    int64_t i = ibase + lane + 32 * q;
+    pi[q] = pos[i < i_hi ? i : i_hi - 1];
+    ax[q] = ay[q] = az[q] = 0.f;
+  }
+  const int64_t jb = (n * warp) / NB_WARPS, je = (n * (warp + 1)) / NB_WARPS;
+  float4 next = (jb + lane < je) ? pos[jb + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t j0 = jb; j0 < je; j0 += 32) {
+    tile[warp][lane] = next;
+    __syncwarp();
+    int64_t jn = j0 + 32 + lane;
+    next = (jn < je) ? pos[jn] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 16
+    for (int k = 0; k < 32; ++k) {
+      float4 pj = tile[warp][k];
+#pragma unroll
+      for (int q = 0; q < NB_IPT; ++q) nb_interact(pi[q], pj, eps2, ax[q], ay[q], az[q]);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int q = 0; q < NB_IPT; ++q) {
+    part[warp][0][lane + 32 * q] = ax[q];
+    part[warp][1][lane + 32 * q] = ay[q];
+    part[warp][2][lane + 32 * q] = az[q];
+  }
+  __syncthreads();
+  if (threadIdx.x < NB_IBLOCK) {
+    int64_t i = ibase + threadIdx.x;
+    if (i < i_hi) {
+      float sx = 0.f, sy = 0.f, sz = 0.f;
+#pragma unroll
+      for (int w = 0; w < NB_WARPS; ++w) {
+        sx += part[w][0][threadIdx.x];
+        sy += part[w][1][threadIdx.x];
+        sz += part[w][2][threadIdx.x];
+      }
+      float4 v = vel_in[i - i_lo];
+      v.x = fmaf(dt, sx, v.x);
+      v.y = fmaf(dt, sy, v.y);
+      v.z = fmaf(dt, sz, v.z);
+      vel[i - i_lo] = v;
+    }
+  }
+}
+
+__global__ void nbody_drift_kernel(const float4* p_in, const float4* __restrict__ v, float4* p,
+                                   int64_t count, float dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = p_in[i], b = v[i];
+    a.x = fmaf(dt, b.x, a.x);
+    a.y = fmaf(dt, b.y, a.y);
+    a.z = fmaf(dt, b.z, a.z);
+    p[i] = a;
+  }
+}
+
+}  // namespace cq
+
+using namespace cq;
+
+#define CQ_GET_STREAM(dev, s)                                               \
+  CQ_TRY(ensure_device(dev));                                               \
+  cudaStream_t st = stream_of(dev, s);                                      \
+  CQ_REQUIRE(st != nullptr, "bad stream %d", s);                            \
+  CQ_CHECK_CUDA(cudaSetDevice(dev));                                        \
+  DeviceState* ds = device_state(dev);                                      \
+  (void)ds;
+
+extern "C" {
+
+int cq_fill(int device, int stream, int kind, const cq_view_t* dst, const cq_box_t* box,
+            const cq_box_t* extent, int mode, double value, int64_t ivalue) {
+  CQ_GET_STREAM(device, stream);
+  int64_t vol = box_volume(*box);
+  if (vol <= 0) return CQ_OK;
+  int grid = grid_for(vol, 256, ds->sm_count, 8);
+  if (kind == CQ_F64) {
+    fill_kernel<double><<<grid, 256, 0, st>>>(*dst, *box, *extent, mode, mode == 0 ? 0.0 : value);
+  } else if (kind == CQ_F32) {
+    fill_kernel<float><<<grid, 256, 0, st>>>(*dst, *box, *extent, mode,
+                                             mode == 0 ? 0.f : (float)value);
+  } else {
+    fill_kernel<long long><<<grid, 256, 0, st>>>(*dst, *box, *extent, mode, mode == 0 ? 0LL : (long long)ivalue);
+  }
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_saxpy(int device, int stream, int kind, double alpha, int64_t ialpha, const void* x,
+             const void* y, void* z, int64_t n) {
+  CQ_GET_STREAM(device, stream);
+  if (n <= 0) return CQ_OK;
+  if (kind == CQ_I64) {
+    saxpy_i64_kernel<<<grid_for(n, 256, ds->sm_count, 8), 256, 0, st>>>(
+        (long long)ialpha, (const long long*)x, (const long long*)y, (long long*)z, n);
+    CQ_CHECK_LAUNCH();
+    return CQ_OK;
+  }
+  bool aligned = (((uintptr_t)x | (uintptr_t)y | (uintptr_t)z) & 15) == 0;
+  CQ_REQUIRE(aligned, "cq_saxpy: operands must be 16-byte aligned");
+  int per = (kind == CQ_F32) ? 4 : 2;
+  int64_t vec = n / per;
+  // persistent-style grid: 148 SMs x 8 blocks x 256 threads, 2 vectors per trip
+  int grid = grid_for((vec + 1) / 2, 256, ds->sm_count, 8);
+  if (kind == CQ_F32)
+    saxpy_kernel<float><<<grid, 256, 0, st>>>((float)alpha, (const float*)x, (const float*)y, (float*)z, n);
+  else
+    saxpy_kernel<double><<<grid, 256, 0, st>>>(alpha, (const double*)x, (const double*)y, (double*)z, n);
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_wave5(int device, int stream, int kind, const cq_view_t* u, const cq_view_t* upr,
+             const cq_view_t* out, const cq_box_t* box, const cq_box_t* extent, double c,
+             double k2, double k4) {
+  CQ_GET_STREAM(device, stream);
+  CQ_REQUIRE(kind == CQ_F32 || kind == CQ_F64, "cq_wave5: float kinds only");
+  int64_t vol = box_volume(*box);
+  if (vol <= 0) return CQ_OK;
+  const int64_t H = extent->hi[1], W = extent->hi[2];
+  const int eb = kind == CQ_F32 ? 4 : 8;
+  const int V = 16 / eb;
+  bool rows_ok = box->hi[0] - box->lo[0] == 1 && box->lo[2] == 0 && box->hi[2] == W && W % V == 0;
+  for (const cq_view_t* v : {u, upr, out}) {
+    rows_ok = rows_ok && ((uintptr_t)v->ptr % 16 == 0) && v->stride[1] % V == 0 && v->alloc.lo[2] == 0 &&
+              v->stride[2] == 1;
+  }
+  if (rows_ok) {
+    constexpr int RB = 32;
+    int64_t rows = box->hi[1] - box->lo[1];
+    dim3 grid((unsigned)((W / V + 255) / 256), (unsigned)((rows + RB - 1) / RB));
+    if (kind == CQ_F32)
+      wave5_rows_kernel<float, RB><<<grid, 256, 0, st>>>(*u, *upr, *out, box->lo[1], box->hi[1], H, W,
+                                                         (float)c, (float)k2, (float)k4);
+    else
+      wave5_rows_kernel<double, RB><<<grid, 256, 0, st>>>(*u, *upr, *out, box->lo[1], box->hi[1], H, W,
+                                                          c, k2, k4);
+  } else {
+    int grid = grid_for(vol, 256, ds->sm_count, 8);
+    if (kind == CQ_F32)
+      wave5_cell_kernel<float><<<grid, 256, 0, st>>>(*u, *upr, *out, *box, H, W, (float)c, (float)k2,
+                                                     (float)k4);
+    else
+      wave5_cell_kernel<double><<<grid, 256, 0, st>>>(*u, *upr, *out, *box, H, W, c, k2, k4);
+  }
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_expr_eval(int device, int stream, const cq_expr_t* expr) {
+  CQ_GET_STREAM(device, stream);
+  int64_t vol = box_volume(expr->box);
+  if (vol <= 0) return CQ_OK;
+  CQ_REQUIRE(expr->n_out >= 1 && expr->n_out <= CQ_EXPR_MAX_OUT, "cq_expr_eval: bad n_out");
+  unsigned long long* flag = (unsigned long long*)ds->error_flag;
+  int grid = grid_for(vol, 128, ds->sm_count, 16);
+  if (expr->kind == CQ_F64) expr_kernel<double><<<grid, 128, 0, st>>>(*expr, flag);
+  else if (expr->kind == CQ_F32) expr_kernel<float><<<grid, 128, 0, st>>>(*expr, flag);
+  else expr_kernel<long long><<<grid, 128, 0, st>>>(*expr, flag);
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_error_flag(int device, int* code, int64_t point[CQ_MAX_DIMS], int clear) {
+  CQ_TRY(ensure_device(device));
+  DeviceState* ds = device_state(device);
+  CQ_CHECK_CUDA(cudaSetDevice(device));
+  unsigned long long buf[4];
+  CQ_CHECK_CUDA(cudaMemcpy(buf, ds->error_flag, sizeof(buf), cudaMemcpyDeviceToHost));
+  // "no error" is the all-ones key written at device setup and on clear
+  if (buf[0] == ~0ull) {
+    *code = 0;
+  } else {
+    *code = (int)(buf[0] & 15ull);
+    memcpy(point, &buf[1], 3 * sizeof(int64_t));
+  }
+  if (clear) {
+    unsigned long long reset[4] = {~0ull, 0, 0, 0};
+    CQ_CHECK_CUDA(cudaMemcpy(ds->error_flag, reset, sizeof(reset), cudaMemcpyHostToDevice));
+  }
+  return CQ_OK;
+}
+
+int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const float* vel_in,
+                  float* vel, int64_t i_lo, int64_t i_hi, float eps2, float dt) {
+  CQ_GET_STREAM(device, stream);
+  if (i_hi <= i_lo) return CQ_OK;
+  int64_t blocks = (i_hi - i_lo + NB_IBLOCK - 1) / NB_IBLOCK;
+  nbody_kick_kernel<<<(unsigned)blocks, NB_WARPS * 32, 0, st>>>(
+      (const float4*)pos, n, (const float4*)vel_in, (float4*)vel, i_lo, i_hi, eps2, dt);
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_nbody_drift(int device, int stream, const float* p_in, const float* v, float* p,
+                   int64_t count, float dt) {
+  CQ_GET_STREAM(device, stream);
+  if (count <= 0) return CQ_OK;
+  nbody_drift_kernel<<<grid_for(count, 256, ds->sm_count, 8), 256, 0, st>>>(
+      (const float4*)p_in, (const float4*)v, (float4*)p, count, dt);
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+}  // extern "C"

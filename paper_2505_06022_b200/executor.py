@@ -1,0 +1,1070 @@
+"""The B200 executor: ``run(plan) -> RunResult`` -- the reference's replaced
+seam (pkg/src/clusterq/simulator.py:101-224).
+
+Same inputs and result shape as the reference simulator, but every data-plane
+operation is real:
+
+* each plan node is a GPU (``Placement``): in one process, node ``k`` runs on
+  device ``k % ndev``; under ``torchrun`` node ``k`` is rank ``k`` (one process
+  per GPU, NCCL between ranks -- Celerity's own model, where every rank plans
+  the whole program and executes its own commands);
+* per (node, buffer) one HBM allocation covering the bounding box of every
+  region the node touches;
+* Execute -> a kernel launch (see ``lowering``); Push/AwaitPush -> NCCL
+  send/recv inside a group, or a DMA copy (same process, NVLink peer copy
+  between devices); host-initialised data (version 1, no producer,
+  scheduler.py:128-131) is materialised directly on the destination instead
+  of being shipped out of node 0;
+* final gather -> device-to-host copies of each final piece from its
+  lowest-id holder (simulator.py:210-222);
+* the trace carries CUDA-event times (seconds, as exact ``Fraction``) so
+  ``account_energy`` works unchanged; NVML energy is measured around the run.
+
+Ordering: commands are walked in the reference's Kahn order (lowest ready id
+first, simulator.py:108-126).  Local memory hazards are tracked per (node,
+buffer) region (RAW/WAR/WAW) and turned into cross-stream event waits, so
+independent work overlaps: the rows of an Execute that do not read freshly
+received halo cells launch on the compute stream immediately, the dependent
+rows go to a high-priority stream after the receive.  Transfers are grouped
+between consecutive Executes of the global order (identically on every rank),
+and a send and its receive are always posted in the same group.
+"""
+
+import ctypes
+import heapq
+import os
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .errors import EvalError, MapperViolationError, ValidationError
+from .lowering import bind_task
+from .model import AccessMode, NativeKernel, apply_mapper
+from .region import Box, Region
+from .scheduler import AwaitPushCommand, ExecuteCommand, Plan, PushCommand
+
+# --------------------------------------------------------------- result types
+
+
+@dataclass(frozen=True)
+class LinkModel:
+    """Accepted for API compatibility with the reference (simulator.py:35-47);
+    the B200 executor measures real transfer times instead of modelling them."""
+
+    latency_s: float = 1e-6
+    bandwidth_bytes_per_s: float = 1e9
+
+    def __post_init__(self):
+        if self.latency_s < 0:
+            raise ValidationError("link latency must be nonnegative")
+        if self.bandwidth_bytes_per_s <= 0:
+            raise ValidationError("link bandwidth must be positive")
+
+    def transfer_time(self, nbytes: int) -> Fraction:
+        return Fraction(self.latency_s) + Fraction(nbytes) / Fraction(self.bandwidth_bytes_per_s)
+
+
+@dataclass
+class TraceEvent:
+    kind: str  # "execute" | "push" | "await_push"
+    node: int
+    command_id: int
+    start: Fraction
+    duration: Fraction
+    bytes: int = 0
+    frequency_ghz: Optional[float] = None
+    task_id: Optional[int] = None
+    task_name: Optional[str] = None
+    label: str = ""
+
+    @property
+    def finish(self) -> Fraction:
+        return self.start + self.duration
+
+
+@dataclass
+class RunResult:
+    buffers: dict
+    trace: list
+    makespan: Fraction
+    plan: Plan
+    measured: dict = field(default_factory=dict)  # NVML energy, device seconds
+
+
+def trace_to_chrome(trace) -> list:
+    """Chrome trace-viewer events, microseconds (simulator.py:227-246)."""
+    lanes = {"execute": 0, "push": 1, "await_push": 2}
+    out = []
+    for ev in trace:
+        args = {"kind": ev.kind, "command": ev.command_id}
+        if ev.frequency_ghz is not None:
+            args["frequency_ghz"] = ev.frequency_ghz
+        if ev.bytes:
+            args["bytes"] = ev.bytes
+        out.append({"name": ev.label or ev.kind, "ph": "X", "pid": ev.node, "tid": lanes[ev.kind],
+                    "ts": float(ev.start * 1_000_000), "dur": float(ev.duration * 1_000_000),
+                    "args": args})
+    return out
+
+
+# ------------------------------------------------------------------ placement
+
+@dataclass(frozen=True)
+class Placement:
+    """node -> (rank, device).  ``world``/``rank`` describe the process group;
+    ``devices`` are this process's CUDA devices."""
+
+    world: int
+    rank: int
+    devices: tuple
+
+    def rank_of(self, node: int, node_count: int) -> int:
+        if self.world == 1:
+            return 0
+        return node * self.world // max(node_count, self.world)
+
+    def device_of(self, node: int, node_count: int) -> int:
+        if self.world == 1:
+            return self.devices[node % len(self.devices)]
+        return self.devices[0]
+
+    def is_local(self, node: int, node_count: int) -> bool:
+        return self.rank_of(node, node_count) == self.rank
+
+
+_dist_state = {"placement": None, "nccl": False}
+
+
+def local_placement() -> Placement:
+    """Placement of this process: the torchrun rank if NCCL was initialised
+    via ``init_distributed``, else all visible GPUs in one process."""
+    if _dist_state["placement"] is not None:
+        return _dist_state["placement"]
+    n = ctypes.c_int32()
+    N.call("cq_device_count", ctypes.byref(n))
+    if n.value < 1:
+        raise ValidationError("no CUDA device visible")
+    return Placement(1, 0, tuple(range(n.value)))
+
+
+def init_distributed(rank: int, world: int, device: int, broadcast_id=None) -> Placement:
+    """Create this rank's NCCL communicator (one rank per GPU).
+
+    ``broadcast_id(bytes_or_None) -> bytes`` distributes rank 0's NCCL unique
+    id; by default it uses ``torch.distributed`` (already initialised, any
+    backend) purely as plumbing."""
+    if broadcast_id is None:
+        def broadcast_id(blob):
+            import torch.distributed as dist
+            box = [blob]
+            dist.broadcast_object_list(box, src=0)
+            return box[0]
+    uid = None
+    if rank == 0:
+        buf = ctypes.create_string_buffer(128)
+        N.call("cq_nccl_unique_id", buf)
+        uid = buf.raw
+    uid = broadcast_id(uid)
+    N.call("cq_init_device", device)
+    if world > 1:
+        N.call("cq_nccl_init", device, world, rank, uid)
+        _dist_state["nccl"] = True
+    pl = Placement(world, rank, (device,))
+    _dist_state["placement"] = pl
+    return pl
+
+
+def shutdown_distributed():
+    if _dist_state["nccl"]:
+        N.call("cq_nccl_destroy")
+    _dist_state.update(placement=None, nccl=False)
+
+
+# ---------------------------------------------------------------- host memory
+
+_pinned = {}
+
+
+def _pin(arr: np.ndarray):
+    """Page-lock a host array once (cached by address) for async DMA."""
+    if arr.nbytes < (1 << 20):
+        return
+    key = (arr.ctypes.data, arr.nbytes)
+    if key in _pinned:
+        return
+    N.call("cq_host_register", ctypes.c_void_p(arr.ctypes.data), arr.nbytes)
+    _pinned[key] = arr  # keep alive while registered
+
+
+def release_pinned():
+    for (ptr, _n), _a in list(_pinned.items()):
+        N.call("cq_host_unregister", ctypes.c_void_p(ptr))
+    _pinned.clear()
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A page-locked host array (for inputs / outputs of repeated runs)."""
+    arr = np.empty(shape, dtype=dtype)
+    _pin(arr)
+    return arr
+
+
+# ------------------------------------------------------------ region helpers
+
+def _pad(box: Box):
+    """3-D padded bounds (leading unit axes)."""
+    pad = 3 - box.dims
+    return (0,) * pad + box.mins, (1,) * pad + box.maxs
+
+
+def _cbox(box: Box) -> N.CqBox:
+    return N.box3(box.mins, box.maxs)
+
+
+def _bbox_union(boxes):
+    boxes = [b for b in boxes if b is not None]
+    if not boxes:
+        return None
+    lo = tuple(min(b.mins[k] for b in boxes) for k in range(boxes[0].dims))
+    hi = tuple(max(b.maxs[k] for b in boxes) for k in range(boxes[0].dims))
+    return Box(lo, hi)
+
+
+class _View:
+    """One (node, buffer) HBM allocation."""
+
+    __slots__ = ("node", "device", "buffer", "box", "ptr", "c", "itemsize", "nbytes")
+
+    def __init__(self, node, device, buffer, box, itemsize):
+        self.node, self.device, self.buffer, self.box = node, device, buffer, box
+        self.itemsize = itemsize
+        lo, hi = _pad(box)
+        shape = [h - l for l, h in zip(lo, hi)]
+        self.nbytes = shape[0] * shape[1] * shape[2] * itemsize
+        p = ctypes.c_void_p()
+        N.call("cq_malloc", device, max(self.nbytes, 16), ctypes.byref(p))
+        self.ptr = p.value
+        v = N.CqView()
+        v.ptr = self.ptr
+        v.alloc.lo[:] = lo
+        v.alloc.hi[:] = hi
+        v.stride[:] = [shape[1] * shape[2], shape[2], 1]
+        self.c = v
+
+    def free(self):
+        if self.ptr:
+            N.call("cq_free", self.device, ctypes.c_void_p(self.ptr))
+            self.ptr = None
+
+    def addr(self, point):
+        """Device address of global cell ``point`` (unpadded)."""
+        lo, _ = _pad(self.box)
+        p = (0,) * (3 - len(point)) + tuple(point)
+        off = sum((a - b) * s for a, b, s in zip(p, lo, self.c.stride))
+        return self.ptr + off * self.itemsize
+
+
+# ------------------------------------------------------------- hazard tracker
+
+class _Hazards:
+    """Per (node, buffer) list of recent accesses -> events to wait on.
+
+    An access is (region, write?, stream key, event).  A new op on stream S
+    waits for every conflicting access (RAW, WAR, WAW) issued on another
+    stream; same-stream order is implicit.  Entries covered by a newer write,
+    or by a newer access on the same stream, can never be the binding
+    constraint again and are dropped."""
+
+    def __init__(self):
+        self.log = {}
+
+    def waits(self, accesses, skey):
+        out = {}
+        for node, buf, region, write in accesses:
+            for r, w, sk, ev in self.log.get((node, buf), ()):
+                if sk == skey or not (write or w):
+                    continue
+                if region.overlaps(r):
+                    out[ev] = sk
+        return out
+
+    def record(self, accesses, skey, event):
+        for node, buf, region, write in accesses:
+            key = (node, buf)
+            kept = []
+            for entry in self.log.get(key, ()):
+                r, w, sk, ev = entry
+                if (write or sk == skey) and region.contains_region(r):
+                    continue
+                kept.append(entry)
+            kept.append((region, write, skey, event))
+            self.log[key] = kept
+
+
+# ------------------------------------------------------------------ the run
+
+def kahn_order(plan: Plan) -> list:
+    """Lowest-ready-id-first topological order (simulator.py:108-126);
+    raises ValidationError on a cycle (simulator.py:204-206)."""
+    cached = getattr(plan, "_cq_order", None)
+    if cached is not None and cached[0] == len(plan.commands):
+        return cached[1]
+    indeg = {c.id: len(c.deps) for c in plan.commands}
+    users = {c.id: [] for c in plan.commands}
+    for c in plan.commands:
+        for d in c.deps:
+            users[d].append(c.id)
+    heap = [cid for cid, d in indeg.items() if d == 0]
+    heapq.heapify(heap)
+    order = []
+    while heap:
+        cid = heapq.heappop(heap)
+        order.append(cid)
+        for u in users[cid]:
+            indeg[u] -= 1
+            if indeg[u] == 0:
+                heapq.heappush(heap, u)
+    if len(order) != len(plan.commands):
+        stuck = sorted(cid for cid, d in indeg.items() if d > 0)
+        raise ValidationError(f"command graph has a cycle involving ids {stuck}")
+    plan._cq_order = (len(plan.commands), order)
+    return order
+
+
+class _Run:
+    def __init__(self, plan: Plan, placement: Placement, gather: str, out: Optional[dict],
+                 trace: bool, energy: bool):
+        self.plan = plan
+        self.pl = placement
+        self.gather = gather
+        self.out_arrays = out or {}
+        self.want_trace = trace
+        self.want_energy = energy
+        self.buffers = plan.graph.buffers
+        self.by_id = {c.id: c for c in plan.commands}
+        self.nodes = plan.node_count
+        self.local_nodes = [n for n in range(self.nodes) if placement.is_local(n, self.nodes)]
+        self.devices = sorted({placement.device_of(n, self.nodes) for n in self.local_nodes})
+        self.views = {}
+        self.scratch = []
+        self.events = []
+        self.free_events = {}
+        self.haz = _Hazards()
+        self.bindings = {}
+        self.trace_marks = []   # (cmd, kind, node, device, [(ev0, ev1)], bytes)
+        self.host_init = {}
+
+    # ---- small helpers -------------------------------------------------
+    def dev(self, node):
+        return self.pl.device_of(node, self.nodes)
+
+    def local(self, node):
+        return self.pl.is_local(node, self.nodes)
+
+    def rank(self, node):
+        return self.pl.rank_of(node, self.nodes)
+
+    def event(self, device, timing=False):
+        pool = self.free_events.setdefault((device, timing), [])
+        if pool:
+            ev = pool.pop()
+        else:
+            h = ctypes.c_uint64()
+            N.call("cq_event_create", device, 1 if timing else 0, ctypes.byref(h))
+            ev = h.value
+        self.events.append((device, timing, ev))
+        return ev
+
+    def issue(self, device, stream, accesses, fn):
+        """Run ``fn`` on (device, stream) after the hazards it depends on.
+        Returns (start, stop) events; ``start`` is None unless tracing."""
+        skey = (device, stream)
+        for ev, _sk in self.haz.waits(accesses, skey).items():
+            N.call("cq_stream_wait_event", device, stream, ctypes.c_uint64(ev))
+        start = None
+        if self.want_trace:
+            start = self.event(device, timing=True)
+            N.call("cq_event_record", ctypes.c_uint64(start), device, stream)
+        fn()
+        stop = self.event(device, timing=self.want_trace)
+        N.call("cq_event_record", ctypes.c_uint64(stop), device, stream)
+        self.haz.record(accesses, skey, stop)
+        return start, stop
+
+    # ---- allocation ----------------------------------------------------
+    def allocate(self):
+        touch = {}
+        for c in self.plan.commands:
+            if isinstance(c, ExecuteCommand):
+                for _a, buf, reg in c.reads:
+                    touch.setdefault((c.node, buf), []).append(reg.bounding_box())
+                for _a, buf, reg, _v in c.writes:
+                    touch.setdefault((c.node, buf), []).append(reg.bounding_box())
+            elif isinstance(c, PushCommand):
+                bb = c.region.bounding_box()
+                touch.setdefault((c.src, c.buffer), []).append(bb)
+                touch.setdefault((c.dst, c.buffer), []).append(bb)
+        for name, entries in self.plan.final_locations.items():
+            for reg, _v, holders in entries:
+                touch.setdefault((min(holders), name), []).append(reg.bounding_box())
+        for (node, buf), boxes in sorted(touch.items()):
+            if not self.local(node):
+                continue
+            bb = _bbox_union(boxes)
+            if bb is None:
+                continue
+            b = self.buffers[buf]
+            self.views[(node, buf)] = _View(node, self.dev(node), buf, bb, b.itemsize)
+
+    # ---- host-initialised data -----------------------------------------
+    def host_array(self, buf):
+        """Host copy of a buffer's initial contents (array inits by reference)."""
+        arr = self.host_init.get(buf)
+        if arr is None:
+            b = self.buffers[buf]
+            arr = b.init.materialize(b.extent, b.element_kind)
+            if b.init.kind in ("array", "values"):
+                arr = np.ascontiguousarray(arr)
+                _pin(arr)
+            self.host_init[buf] = arr
+        return arr
+
+    def materialize(self, node, buf, region, stream):
+        """Write host-initialised contents of ``region`` into node's view."""
+        b = self.buffers[buf]
+        view = self.views[(node, buf)]
+        dev = view.device
+        init = b.init
+        kind = N.KIND_CODE[b.element_kind]
+        ext = _cbox(b.extent)
+
+        def go():
+            for box in region.boxes:
+                cb = _cbox(box)
+                if init.kind in ("array", "values"):
+                    arr = self.host_array(buf)
+                    N.call("cq_copy_box_h2d", dev, stream, b.itemsize, ctypes.byref(view.c),
+                           ctypes.c_void_p(arr.ctypes.data), ctypes.byref(ext), ctypes.byref(cb))
+                else:
+                    mode = {"iota": 1, "constant": 2}.get(init.kind, 0)
+                    val = float(init.value) if init.kind == "constant" else 0.0
+                    ival = int(init.value) if (init.kind == "constant" and b.element_kind == "int64") else 0
+                    N.call("cq_fill", dev, stream, kind, ctypes.byref(view.c), ctypes.byref(cb),
+                           ctypes.byref(ext), mode, ctypes.c_double(val), ival)
+        return self.issue(dev, stream, [(node, buf, region, True)], go)
+
+    def seed_node0(self):
+        """Node 0 holds version 1 of every initialised buffer; materialise it
+        over node 0's allocation (only what node 0 itself touches)."""
+        if not self.local(0):
+            return
+        for (node, buf), view in self.views.items():
+            if node != 0 or not self.buffers[buf].init.is_initialized:
+                continue
+            self.materialize(0, buf, Region.from_box(view.box), N.STREAM_COMM)
+
+    # ---- transfers -------------------------------------------------------
+    def flush_group(self, group):
+        """Issue one group of transfers (all ranks cut groups identically)."""
+        if not group:
+            return
+        nccl_ops = []
+        for push in group:
+            src_l, dst_l = self.local(push.src), self.local(push.dst)
+            if not push.deps:
+                # host-initialised data: the destination materialises it
+                if dst_l:
+                    t = self.materialize(push.dst, push.buffer, push.region, N.STREAM_COMM)
+                    self.mark_transfer(push, push.dst, t)
+                continue
+            if src_l and dst_l:
+                self.local_copy(push)
+            elif src_l or dst_l:
+                nccl_ops.append(push)
+        if nccl_ops:
+            self.nccl_group(nccl_ops)
+
+    def local_copy(self, push):
+        src = self.views[(push.src, push.buffer)]
+        dst = self.views[(push.dst, push.buffer)]
+        dev = dst.device
+        eb = self.buffers[push.buffer].itemsize
+        acc = [(push.src, push.buffer, push.region, False), (push.dst, push.buffer, push.region, True)]
+
+        def go():
+            for box in push.region.boxes:
+                cb = _cbox(box)
+                N.call("cq_copy_box", dev, N.STREAM_COMM, eb, ctypes.byref(dst.c), dst.device,
+                       ctypes.byref(src.c), src.device, ctypes.byref(cb))
+        self.mark_transfer(push, push.dst, self.issue(dev, N.STREAM_COMM, acc, go))
+
+    def nccl_group(self, pushes):
+        """Sends and receives of this rank, posted as one NCCL group."""
+        dev = self.pl.devices[0]
+        accesses = []
+        for p in pushes:
+            if self.local(p.src):
+                accesses.append((p.src, p.buffer, p.region, False))
+            if self.local(p.dst):
+                accesses.append((p.dst, p.buffer, p.region, True))
+        staged = []
+
+        def go():
+            # pack non-contiguous boxes before the group, unpack after it
+            plan_ops = []
+            for p in pushes:
+                eb = self.buffers[p.buffer].itemsize
+                for box in p.region.boxes:
+                    vol = box.volume()
+                    if self.local(p.src):
+                        v = self.views[(p.src, p.buffer)]
+                        ptr = self._contig_ptr(v, box)
+                        if ptr is None:
+                            tmp = self.scratch_alloc(v.device, vol * eb)
+                            N.call("cq_pack_box", v.device, N.STREAM_COMM, eb, ctypes.c_void_p(tmp),
+                                   ctypes.byref(v.c), ctypes.byref(_cbox(box)))
+                            ptr = tmp
+                        plan_ops.append(("send", ptr, vol * eb, self.rank(p.dst)))
+                    if self.local(p.dst):
+                        v = self.views[(p.dst, p.buffer)]
+                        ptr = self._contig_ptr(v, box)
+                        if ptr is None:
+                            tmp = self.scratch_alloc(v.device, vol * eb)
+                            staged.append((v, tmp, box, eb))
+                            ptr = tmp
+                        plan_ops.append(("recv", ptr, vol * eb, self.rank(p.src)))
+            N.call("cq_nccl_group_start")
+            for op, ptr, nbytes, peer in plan_ops:
+                fn = "cq_nccl_send" if op == "send" else "cq_nccl_recv"
+                N.call(fn, dev, N.STREAM_COMM, ctypes.c_void_p(ptr), nbytes, peer)
+            N.call("cq_nccl_group_end")
+            for v, tmp, box, eb in staged:
+                N.call("cq_unpack_box", v.device, N.STREAM_COMM, eb, ctypes.byref(v.c),
+                       ctypes.c_void_p(tmp), ctypes.byref(_cbox(box)))
+        t = self.issue(dev, N.STREAM_COMM, accesses, go)
+        for p in pushes:
+            self.mark_transfer(p, p.src if self.local(p.src) else p.dst, t)
+
+    def _contig_ptr(self, view, box):
+        lo, hi = _pad(box)
+        vlo, vhi = _pad(view.box)
+        k = 0
+        while k < 2 and hi[k] - lo[k] == 1:
+            k += 1
+        for j in range(k + 1, 3):
+            if hi[j] - lo[j] != vhi[j] - vlo[j]:
+                return None
+        return view.addr(box.mins)
+
+    def scratch_alloc(self, device, nbytes):
+        p = ctypes.c_void_p()
+        N.call("cq_malloc", device, max(nbytes, 16), ctypes.byref(p))
+        self.scratch.append((device, p.value))
+        return p.value
+
+    # ---- timing marks for the trace ----------------------------------------
+    def mark_transfer(self, push, node, events):
+        if self.want_trace:
+            start, stop = events
+            self.trace_marks.append((push, node, self.dev(node), start, stop))
+
+    # ---- executes --------------------------------------------------------
+    def execute(self, cmd: ExecuteCommand, awaited):
+        task = self.plan.graph.task(cmd.task_id)
+        binding = self.bindings.get(task.id)
+        if binding is None:
+            binding = self.bindings[task.id] = bind_task(task, self.buffers)
+        node, dev = cmd.node, self.dev(cmd.node)
+        rviews = {}
+        for a in task.accessors:
+            if a.mode is AccessMode.READ:
+                rviews[a.name] = self.views.get((node, a.buffer))
+        wviews = {a.name: self.views[(node, a.buffer)] for a in task.writes()}
+        reads = {name: (buf, reg) for name, buf, reg in cmd.reads}
+
+        # snapshot reads of buffers this task overwrites at non-zero offsets
+        for name in binding.snapshot:
+            buf, reg = reads[name]
+            src = rviews[name]
+            bb = reg.bounding_box()
+            snap = _View(node, dev, buf, bb, src.itemsize)
+            self.scratch.append((dev, snap))
+
+            def go(src=src, snap=snap, reg=reg):
+                for box in reg.boxes:
+                    N.call("cq_copy_box", dev, N.STREAM_COMPUTE, src.itemsize, ctypes.byref(snap.c), dev,
+                           ctypes.byref(src.c), dev, ctypes.byref(_cbox(box)))
+            self.issue(dev, N.STREAM_COMPUTE, [(node, buf, reg, False)], go)
+            rviews[name] = snap
+
+        pieces = self.split(task, cmd, awaited)
+        marks = []
+        for box, dependent in pieces:
+            # only a split chunk sends its halo-dependent rows to the
+            # high-priority stream; an unsplit chunk stays on the compute one
+            stream = N.STREAM_BOUNDARY if dependent and len(pieces) > 1 else N.STREAM_COMPUTE
+            acc = []
+            for a in task.accessors:
+                if a.mode is AccessMode.READ:
+                    if a.name in binding.snapshot:
+                        continue
+                    reg = apply_mapper(a.mapper, box, task.global_range, self.buffers[a.buffer].extent)
+                    acc.append((node, a.buffer, reg, False))
+            for a in task.writes():
+                acc.append((node, a.buffer, Region.from_box(box), True))
+            marks.append(self.issue(dev, stream, acc,
+                                    lambda box=box, stream=stream: self.launch(
+                                        binding, task, cmd, box, dev, stream, rviews, wviews, reads)))
+        if self.want_trace:
+            self.trace_marks.append((cmd, node, dev, marks, None))
+
+    def split(self, task, cmd, awaited):
+        """Cut the chunk along dim 0 into rows that do not read awaited
+        (just-received) cells -- launched at once -- and rows that do."""
+        box = cmd.chunk.box
+        if not awaited or task.is_native:
+            return [(box, bool(awaited))]
+        lo0, hi0 = box.mins[0], box.maxs[0]
+        cuts = {lo0, hi0}
+        for a in task.accessors:
+            if a.mode is not AccessMode.READ or a.buffer not in awaited:
+                continue
+            m = a.mapper
+            radius = getattr(m, "radii", None)
+            if radius is None and type(m).__name__ != "OneToOne":
+                return [(box, True)]
+            r0 = radius[0] if radius else 0
+            for ab in awaited[a.buffer].boxes:
+                for c in (ab.mins[0] - r0, ab.maxs[0] + r0):
+                    if lo0 < c < hi0:
+                        cuts.add(c)
+        edges = sorted(cuts)
+        out = []
+        for a0, b0 in zip(edges, edges[1:]):
+            sub = Box((a0,) + box.mins[1:], (b0,) + box.maxs[1:])
+            dep = False
+            for a in task.accessors:
+                if a.mode is AccessMode.READ and a.buffer in awaited:
+                    img = apply_mapper(a.mapper, sub, task.global_range, self.buffers[a.buffer].extent)
+                    if img.overlaps(awaited[a.buffer]):
+                        dep = True
+                        break
+            out.append((sub, dep))
+        out.sort(key=lambda p: p[1])  # independent pieces first
+        return out
+
+    def launch(self, binding, task, cmd, box, dev, stream, rviews, wviews, reads):
+        kind_name = self.buffers[task.writes()[0].buffer].element_kind
+        kind = N.KIND_CODE[kind_name]
+        if binding.kind == "saxpy":
+            args = binding.args
+            xv, yv, zv = rviews[args["x"]], rviews[args["y"]], wviews[args["out"]]
+            contiguous = all(self._contig_ptr(v, box) is not None for v in (xv, yv, zv))
+            aligned = kind == N.CQ_I64 or all(v.addr(box.mins) % 16 == 0 for v in (xv, yv, zv))
+            if contiguous and aligned:
+                alpha = args["alpha"]
+                N.call("cq_saxpy", dev, stream, kind, ctypes.c_double(float(alpha)),
+                       int(alpha) if kind == N.CQ_I64 else 0,
+                       ctypes.c_void_p(xv.addr(box.mins)), ctypes.c_void_p(yv.addr(box.mins)),
+                       ctypes.c_void_p(zv.addr(box.mins)), box.volume())
+                return
+            # non-contiguous chunk (n-D body on a partial range): interpreter
+            binding = self.bindings.get(("expr", task.id))
+            if binding is None:
+                binding = self.bindings[("expr", task.id)] = _expr_binding(task, self.buffers)
+        if binding.kind == "wave5":
+            a = binding.args
+            uacc = next(x for x in task.accessors if x.name == a["u"])
+            ext = _cbox(self.buffers[uacc.buffer].extent)
+            N.call("cq_wave5", dev, stream, kind, ctypes.byref(rviews[a["u"]].c),
+                   ctypes.byref(rviews[a["upr"]].c), ctypes.byref(wviews[a["out"]].c),
+                   ctypes.byref(_cbox(box)), ctypes.byref(ext), ctypes.c_double(a["c"]),
+                   ctypes.c_double(a["k2"]), ctypes.c_double(a["k4"]))
+            return
+        if binding.kind == "native":
+            self.launch_native(binding, task, box, dev, stream, rviews, wviews)
+            return
+        self.launch_expr(binding, task, cmd, box, dev, stream, rviews, wviews, reads)
+
+    def launch_native(self, binding, task, box, dev, stream, rviews, wviews):
+        name = binding.args["name"]
+        lo, hi = box.mins[0], box.maxs[0]
+        if name == "nbody.kick":
+            pos = rviews["pos"]
+            n = self.buffers[next(a.buffer for a in task.accessors if a.name == "pos")].extent.maxs[0]
+            N.call("cq_nbody_kick", dev, stream, ctypes.c_void_p(pos.addr((0, 0))), n,
+                   ctypes.c_void_p(rviews["vel_in"].addr((lo, 0))),
+                   ctypes.c_void_p(wviews["vel"].addr((lo, 0))), lo, hi,
+                   ctypes.c_float(task.params["eps2"]), ctypes.c_float(task.params["dt"]))
+        elif name == "nbody.drift":
+            N.call("cq_nbody_drift", dev, stream, ctypes.c_void_p(rviews["pos_in"].addr((lo, 0))),
+                   ctypes.c_void_p(rviews["vel"].addr((lo, 0))),
+                   ctypes.c_void_p(wviews["pos"].addr((lo, 0))), hi - lo,
+                   ctypes.c_float(task.params["dt"]))
+        elif name == "sgemm":
+            a, b, c = rviews["a"], rviews["b"], wviews["c"]
+            k = a.box.maxs[1] - a.box.mins[1]
+            ncols = box.maxs[1] - box.mins[1]
+            variant = {"ffma": N.SGEMM_FFMA, "3xtf32": N.SGEMM_3XTF32}.get(
+                binding.args["variant"] or _default_sgemm(), N.SGEMM_FFMA)
+            N.call("cq_sgemm", dev, stream, variant, ctypes.c_void_p(a.addr((lo, 0))), a.c.stride[1],
+                   ctypes.c_void_p(b.addr((0, box.mins[1]))), b.c.stride[1],
+                   ctypes.c_void_p(c.addr((lo, box.mins[1]))), c.c.stride[1], hi - lo, ncols, k)
+        else:
+            raise ValidationError(f"no native kernel '{name}'")
+
+    def launch_expr(self, binding, task, cmd, box, dev, stream, rviews, wviews, reads):
+        if binding.kind != "expr":
+            binding = _expr_binding(task, self.buffers)
+        kind_name = self.buffers[task.writes()[0].buffer].element_kind
+        X = N.CqExpr()
+        X.kind = N.KIND_CODE[kind_name]
+        X.dims = task.dims
+        X.box = _cbox(box)
+        accs = {a.name: a for a in task.accessors}
+        view_index = {}
+        code_ops, code_args, consts = [], [], []
+        slots = []
+        X.n_out = len(binding.programs)
+        kpad = 3 - task.dims
+        for o, (wname, prog) in enumerate(binding.programs):
+            X.out[o] = wviews[wname].c
+            X.out_code_begin[o] = len(code_ops)
+            base_const = len(consts)
+            for v in prog.consts:
+                if kind_name == "int64":
+                    consts.append(int(v))
+                else:
+                    consts.append(int(np.float64(v).view(np.int64)))
+            slot_map = {}
+            for si, (acc_name, offs) in enumerate(prog.reads):
+                if acc_name not in view_index:
+                    vi = len(view_index)
+                    view_index[acc_name] = vi
+                slot_map[si] = len(slots)
+                slots.append((view_index[acc_name], offs))
+            for op, arg in prog.code:
+                code_ops.append(op)
+                if op == 0:
+                    code_args.append(base_const + arg)
+                elif op == 1:
+                    code_args.append(kpad + arg)
+                elif op == 2:
+                    code_args.append(slot_map[arg])
+                else:
+                    code_args.append(0)
+            X.out_code_end[o] = len(code_ops)
+        if len(code_ops) > N.MAX_CODE or len(consts) > N.MAX_CONST or len(slots) > N.MAX_SLOTS \
+                or len(view_index) > N.MAX_VIEWS:
+            raise ValidationError(f"task '{task.name}': body too large for the device interpreter")
+        X.n_code = len(code_ops)
+        for i, (op, arg) in enumerate(zip(code_ops, code_args)):
+            X.code_op[i] = op
+            X.code_arg[i] = arg
+        X.n_const = len(consts)
+        for i, v in enumerate(consts):
+            X.consts[i] = v
+        X.n_slots = len(slots)
+        for i, (vi, offs) in enumerate(slots):
+            X.slot_view[i] = vi
+            for j, o in enumerate(offs):
+                X.slot_off[i][j] = o
+        X.n_views = len(view_index)
+        for acc_name, vi in view_index.items():
+            acc = accs[acc_name]
+            b = self.buffers[acc.buffer]
+            X.views[vi] = rviews[acc_name].c
+            X.view_extent[vi] = _cbox(b.extent)
+            X.view_dims[vi] = b.dims
+            # mapper check only where the clamped image may leave the region
+            # (ReadView.read, model.py:442-453)
+            region = reads[acc_name][1]
+            need = False
+            for s_vi, offs in slots:
+                if s_vi != vi:
+                    continue
+                img = _clamped_image(box, offs, b.extent)
+                if img is None or not region.contains_region(Region.from_box(img)):
+                    need = True
+                    break
+            if need:
+                if len(region.boxes) > N.MAX_CHECK:
+                    raise ValidationError(f"task '{task.name}': mapped region of '{acc_name}' has "
+                                          f"too many boxes for the device mapper check")
+                X.view_n_check[vi] = max(1, len(region.boxes))
+                if not region.boxes:
+                    X.view_check[vi][0] = N.box3((0,) * b.dims, (0,) * b.dims)
+                for bi, rb in enumerate(region.boxes):
+                    X.view_check[vi][bi] = _cbox(rb)
+        N.call("cq_expr_eval", dev, stream, ctypes.byref(X))
+
+    # ---- the walk --------------------------------------------------------
+    def run(self):
+        order = kahn_order(self.plan)
+        for d in self.devices:
+            N.call("cq_init_device", d)
+        e0 = {}
+        energy0 = {}
+        if self.want_energy:
+            for d in self.devices:
+                try:
+                    mj = ctypes.c_uint64()
+                    N.call("cq_nvml_energy_mj", d, ctypes.byref(mj))
+                    energy0[d] = mj.value
+                except Exception:
+                    energy0 = {}
+                    break
+        self.allocate()
+        for d in self.devices:
+            ev = self.event(d, timing=True)
+            N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
+            e0[d] = ev
+            for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
+                N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
+        self.seed_node0()
+
+        group = []
+        group_acc = []
+        awaited_by_exec = {}
+        pending_await = {}
+        for cid in order:
+            c = self.by_id[cid]
+            if isinstance(c, ExecuteCommand):
+                self.flush_group(group)
+                group, group_acc = [], []
+                if self.local(c.node):
+                    aw = {}
+                    for d in c.deps:
+                        a = self.by_id[d]
+                        if isinstance(a, AwaitPushCommand) and a.dst == c.node:
+                            aw[a.buffer] = aw[a.buffer].union(a.region) if a.buffer in aw else a.region
+                    self.execute(c, aw)
+            elif isinstance(c, PushCommand):
+                acc = [(c.src, c.buffer, c.region, False), (c.dst, c.buffer, c.region, True)]
+                if any(n == n2 and b == b2 and (w or w2) and r.overlaps(r2)
+                       for n, b, r, w in acc for n2, b2, r2, w2 in group_acc):
+                    self.flush_group(group)
+                    group, group_acc = [], []
+                group.append(c)
+                group_acc.extend(acc)
+            # AwaitPush: its receive was posted with the push (same group)
+        self.flush_group(group)
+
+        for d in self.devices:
+            for s in (N.STREAM_COMPUTE, N.STREAM_BOUNDARY, N.STREAM_COMM):
+                N.call("cq_stream_synchronize", d, s)
+        self.check_errors()
+        result = self.collect()
+        measured = {}
+        if energy0:
+            for d in self.devices:
+                mj = ctypes.c_uint64()
+                N.call("cq_nvml_energy_mj", d, ctypes.byref(mj))
+                measured[f"energy_j_device{d}"] = (mj.value - energy0[d]) / 1000.0
+        trace, makespan = self.build_trace(e0)
+        self.release()
+        return RunResult(buffers=result, trace=trace, makespan=makespan, plan=self.plan,
+                         measured=measured)
+
+    def check_errors(self):
+        for d in self.devices:
+            code = ctypes.c_int32()
+            pt = (ctypes.c_int64 * 3)()
+            N.call("cq_error_flag", d, ctypes.byref(code), pt, 1)
+            if code.value == N.CQ_ERR_EVAL:
+                raise EvalError(f"integer division by zero at id {tuple(pt)}")
+            if code.value == N.CQ_ERR_MAPPER:
+                raise MapperViolationError(f"read at id {tuple(pt)} outside the mapped region")
+
+    # ---- gather ------------------------------------------------------------
+    def collect(self):
+        if self.gather == "none":
+            return {}
+        out = {}
+        root = self.pl.rank == 0
+        pending = []
+        for name, entries in self.plan.final_locations.items():
+            b = self.buffers[name]
+            arr = self.out_arrays.get(name)
+            if arr is None:
+                arr = np.zeros(b.extent.shape, dtype=b.dtype)
+            else:
+                arr[...] = 0
+            init_v1 = b.init.is_initialized
+            for region, version, holders in entries:
+                src = min(holders)
+                if init_v1 and version == 1:
+                    if root or self.gather == "local":
+                        host = self.host_array(name)
+                        for box in region.boxes:
+                            sl = tuple(slice(lo, hi) for lo, hi in zip(box.mins, box.maxs))
+                            arr[sl] = host[sl]
+                    continue
+                if self.local(src) and (root or self.gather == "local"):
+                    view = self.views[(src, name)]
+                    pending.append((view, arr, region))
+                elif self.gather == "root" and (self.local(src) or root):
+                    pending.append(("nccl", src, name, arr, region))
+            out[name] = arr
+        direct = [p for p in pending if p[0] != "nccl"]
+        temp_pins = []
+        for view, arr, region in direct:
+            key = (arr.ctypes.data, arr.nbytes)
+            if arr.nbytes >= (1 << 20) and key not in _pinned and key not in temp_pins:
+                # page-lock fresh result arrays only for the copy (the caller
+                # owns them afterwards); `out=` arrays from pinned_empty stay pinned
+                N.call("cq_host_register", ctypes.c_void_p(arr.ctypes.data), arr.nbytes)
+                temp_pins.append(key)
+            ha = N.box3((0,) * arr.ndim, arr.shape)
+            for box in region.boxes:
+                N.call("cq_copy_box_d2h", view.device, N.STREAM_COMM, view.itemsize,
+                       ctypes.c_void_p(arr.ctypes.data), ctypes.byref(ha), ctypes.byref(view.c),
+                       ctypes.byref(_cbox(box)))
+        remote = [p for p in pending if p[0] == "nccl"]
+        if remote:
+            self.gather_remote(remote)
+        for d in self.devices:
+            N.call("cq_stream_synchronize", d, N.STREAM_COMM)
+        for ptr, _n in temp_pins:
+            N.call("cq_host_unregister", ctypes.c_void_p(ptr))
+        if self.gather == "root" and not root:
+            return {}
+        return out
+
+    def gather_remote(self, items):
+        """Ship final pieces held by other ranks to rank 0 over NCCL."""
+        dev = self.pl.devices[0]
+        ops = []
+        unpack = []
+        for _tag, src, name, arr, region in items:
+            eb = self.buffers[name].itemsize
+            for box in region.boxes:
+                nbytes = box.volume() * eb
+                if self.local(src):
+                    v = self.views[(src, name)]
+                    ptr = self._contig_ptr(v, box)
+                    if ptr is None:
+                        ptr = self.scratch_alloc(v.device, nbytes)
+                        N.call("cq_pack_box", v.device, N.STREAM_COMM, eb, ctypes.c_void_p(ptr),
+                               ctypes.byref(v.c), ctypes.byref(_cbox(box)))
+                    ops.append(("send", ptr, nbytes, 0))
+                else:
+                    ptr = self.scratch_alloc(dev, nbytes)
+                    ops.append(("recv", ptr, nbytes, self.rank(src)))
+                    unpack.append((ptr, arr, box, eb))
+        N.call("cq_nccl_group_start")
+        for op, ptr, nbytes, peer in ops:
+            fn = "cq_nccl_send" if op == "send" else "cq_nccl_recv"
+            N.call(fn, dev, N.STREAM_COMM, ctypes.c_void_p(ptr), nbytes, peer)
+        N.call("cq_nccl_group_end")
+        for ptr, arr, box, eb in unpack:
+            _pin(arr)
+            ha = N.box3((0,) * arr.ndim, arr.shape)
+            dense = N.CqView()
+            dense.ptr = ptr
+            lo, hi = _pad(box)
+            dense.alloc.lo[:] = lo
+            dense.alloc.hi[:] = hi
+            sh = [h - l for l, h in zip(lo, hi)]
+            dense.stride[:] = [sh[1] * sh[2], sh[2], 1]
+            N.call("cq_copy_box_d2h", dev, N.STREAM_COMM, eb, ctypes.c_void_p(arr.ctypes.data),
+                   ctypes.byref(ha), ctypes.byref(dense), ctypes.byref(_cbox(box)))
+
+    # ---- trace -------------------------------------------------------------
+    def build_trace(self, e0):
+        trace = []
+        if not self.want_trace:
+            return trace, Fraction(0)
+
+        def secs(dev, ev):
+            ms = ctypes.c_float()
+            N.call("cq_event_elapsed_ms", ctypes.c_uint64(e0[dev]), ctypes.c_uint64(ev), ctypes.byref(ms))
+            return Fraction(max(ms.value, 0.0)) / 1000
+
+        for item in self.trace_marks:
+            cmd = item[0]
+            if isinstance(cmd, ExecuteCommand):
+                _c, node, dev, marks, _ = item
+                starts = [secs(dev, a) for a, _b in marks]
+                stops = [secs(dev, b) for _a, b in marks]
+                if not starts:
+                    continue
+                t0, t1 = min(starts), max(stops)
+                task = self.plan.graph.task(cmd.task_id)
+                trace.append(TraceEvent("execute", node, cmd.id, t0, t1 - t0,
+                                        frequency_ghz=cmd.frequency_ghz, task_id=cmd.task_id,
+                                        task_name=task.name, label=f"{task.name}#{cmd.task_id} {cmd.chunk.box}"))
+            else:
+                push, node, dev, a, b = item
+                t0, t1 = secs(dev, a), secs(dev, b)
+                trace.append(TraceEvent("push", push.src, push.id, t0, max(t1 - t0, Fraction(0)),
+                                        bytes=push.bytes,
+                                        label=f"{push.buffer} {push.region} n{push.src}->n{push.dst}"))
+                trace.append(TraceEvent("await_push", push.dst, push.id + 1, t1, Fraction(0),
+                                        bytes=push.bytes, label=f"{push.buffer} {push.region} n{push.dst}"))
+        trace.sort(key=lambda e: e.command_id)
+        makespan = max((e.finish for e in trace), default=Fraction(0))
+        return trace, makespan
+
+    def release(self):
+        for v in self.views.values():
+            v.free()
+        for dev, item in self.scratch:
+            if isinstance(item, _View):
+                item.free()
+            else:
+                N.call("cq_free", dev, ctypes.c_void_p(item))
+        for dev, timing, ev in self.events:
+            N.call("cq_event_destroy", ctypes.c_uint64(ev))
+        self.views.clear()
+        self.scratch.clear()
+        self.events.clear()
+
+
+def _clamped_image(box, offs, extent):
+    """Box of clamped read points for ``box`` shifted by ``offs`` (buffer
+    axes are the leading kernel axes, model.py:442-446)."""
+    lo, hi = [], []
+    for j, o in enumerate(offs):
+        e0, e1 = extent.mins[j], extent.maxs[j]
+        a = min(max(box.mins[j] + o, e0), e1 - 1)
+        b = min(max(box.maxs[j] - 1 + o, e0), e1 - 1) + 1
+        if a >= b:
+            return None
+        lo.append(a)
+        hi.append(b)
+    return Box(lo, hi)
+
+
+def _expr_binding(task, buffers):
+    from .lowering import Binding
+    from . import kernel as K
+    progs = tuple((w.name, K.lower(task.body[w.name], task.params, buffers[w.buffer].element_kind))
+                  for w in task.writes())
+    return Binding("expr", {}, progs, frozenset())
+
+
+def _default_sgemm():
+    return os.environ.get("CQ_SGEMM", "ffma")
+
+
+def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
+        out: Optional[dict] = None, trace: bool = True, energy: bool = False,
+        placement: Optional[Placement] = None) -> RunResult:
+    """Execute ``plan`` on B200 GPUs (drop-in for simulator.run).
+
+    gather: "root" (default) -- rank 0 receives full buffers (single process:
+            the caller gets them); "local" -- each rank fills only what it
+            holds; "none" -- results stay on the devices (benchmarking).
+    out:    optional {buffer: ndarray} destinations (e.g. ``pinned_empty``).
+    energy: measure NVML energy per device over the run (``measured``).
+    """
+    if link is not None and not isinstance(link, LinkModel):
+        raise ValidationError("link must be a LinkModel")
+    if gather not in ("root", "local", "none"):
+        raise ValidationError(f"unknown gather mode '{gather}'")
+    pl = placement or local_placement()
+    return _Run(plan, pl, gather, out, trace, energy).run()

@@ -1,0 +1,52 @@
+"""The C-ABI library builds, loads without a GPU and exports exactly the
+entry points include/cq.h declares (no compute calls here)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2505_06022_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    with open(os.path.join(ROOT, "include", "cq.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(cq_\w+)\(", text, re.M)))
+
+
+def test_header_and_binding_agree():
+    assert header_functions() == sorted(N.EXPORTED)
+
+
+def test_library_exports_every_header_symbol():
+    lib = N.load()
+    for name in header_functions():
+        assert hasattr(lib, name), name
+
+
+def test_library_reports_missing_gpu_loudly():
+    """Without a GPU every device call fails with a CUDA status -- there is
+    no silent CPU path."""
+    lib = N.load()
+    n = ctypes.c_int32(-1)
+    status = lib.cq_device_count(ctypes.byref(n))
+    if status == N.CQ_OK and n.value > 0:
+        pytest.skip("a GPU is visible")
+    assert status != N.CQ_OK or n.value == 0
+    with pytest.raises(Exception):
+        import paper_2505_06022_b200 as cq
+        from paper_2505_06022_b200 import workloads as W
+        cq.run(cq.generate_commands(W.saxpy_program(64).graph(), 1))
+
+
+def test_sm100a_code_in_library():
+    """The fatbin carries sm_100a SASS (cross-compiled here)."""
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", N.LIB_PATH],
+                         capture_output=True, text=True)
+    assert out.returncode == 0
+    assert "sm_100a" in out.stdout
