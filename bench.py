@@ -1,0 +1,519 @@
+#!/usr/bin/env python
+"""BASELINE benchmark: "GB/s (or GFLOP/s) per kernel at 1/2/4/8 B200, %
+roofline; J/iteration vs SM clock" (BASELINE.json).
+
+Headline workload = BASELINE configs[1]: the 2-D wave_sim 5-point stencil,
+fp32, 100 time steps, neighborhood(1,1) halo exchange, weak-scaled at
+16384 x 16384 cells per GPU (global 16384*N x 16384).  One bench *step* is
+one full 100-time-step simulation through the reference-shaped API:
+Buffer/Task/TaskGraph -> generate_commands -> B200 executor.
+
+* value     -- device-resident: the plan re-executed on data already in HBM
+               (Session.execute(upload=False)), CUDA events, max over ranks.
+* e2e       -- the public call ``run(plan)`` with pinned host input arrays
+               (H2D inside the timed region) and the result read back to host.
+* roofline  -- the dominant kernel (cq_wave5 rows kernel): 12 algorithmic
+               bytes per cell per launch / its CUDA-event launch time, against
+               MEASURED_PEAKS.json hbm_gbs.
+* kernels   -- the other BASELINE workloads at this N (SAXPY, N-body, sgemm).
+* energy    -- NVML J/iteration per kernel at the running SM clock.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SIZE = 16384
+WAVE_STEPS = 100
+C = 0.25
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ distributed
+
+class Dist:
+    def __init__(self, gpus):
+        self.world = _env_int("WORLD_SIZE", 1)
+        self.rank = _env_int("RANK", 0)
+        self.local_rank = _env_int("LOCAL_RANK", 0)
+        self.gpus = gpus
+        self.torch = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
+            self.torch = torch
+            self.dist = dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([float(x)], device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def min(self, x):
+        return -self.max(-x)
+
+    def sum(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([float(x)], device="cuda")
+        self.dist.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# -------------------------------------------------------------- wave program
+
+def wave_inputs(h, w, rows):
+    """Gaussian pulse, written only for the rows this rank
+    touches (the rest of the big host arrays stays virtual)."""
+    from paper_2505_06022_b200 import executor as E
+    from paper_2505_06022_b200.region import Box
+    box = Box((rows[0], 0), (rows[1], w))
+    u0 = E.pinned_empty((h, w), np.float32, box)
+    i = np.arange(rows[0], rows[1], dtype=np.float64)[:, None] - h / 2
+    j = np.arange(w, dtype=np.float64)[None, :] - w / 2
+    s = (w / 16.0) ** 2
+    u0[rows[0]:rows[1]] = np.exp(-(i * i + j * j) / (2 * s)).astype(np.float32)
+    up0 = E.pinned_empty((h, w), np.float32, box)
+    up0[rows[0]:rows[1]] = u0[rows[0]:rows[1]]
+    return u0, up0
+
+
+def bench_wave(args, dist, placement, peaks):
+    import paper_2505_06022_b200 as cq
+    from paper_2505_06022_b200 import executor as E
+    from paper_2505_06022_b200 import workloads as W
+    from paper_2505_06022_b200.region import Box
+
+    world, rank = dist.world, dist.rank
+    H, Wd, steps = args.size * world, args.size, args.wave_steps
+    lo, hi = rank * args.size, (rank + 1) * args.size
+    rows = (max(lo - 1, 0), min(hi + 1, H))
+    u0, up0 = wave_inputs(H, Wd, rows)
+    prog = W.wave_program(H, Wd, steps=steps, kind="float32", c=C, u0=u0, up0=up0)
+    t0 = time.perf_counter()
+    plan = cq.generate_commands(prog.graph(), world)
+    plan_s = time.perf_counter() - t0
+
+    # ---- device-resident value ------------------------------------------
+    sess = E.Session(plan, placement, trace=True)
+    sess.execute(upload=True)
+    sess.synchronize()
+    sess.recycle()
+    for _ in range(args.warmup):
+        sess.execute(upload=False)
+        sess.synchronize()
+        sess.recycle()
+    dist.barrier()
+    dev = placement.devices[0]
+    with ClockSampler(dev) as clocks:
+        m0 = sess.mark()
+        for _ in range(args.steps):
+            sess.execute(upload=False)
+        m1 = sess.mark()
+        sess.synchronize()
+    dev_ms = max(sess.elapsed_ms(m0[d], m1[d]) for d in sess.devices)
+    wave_launches = [x for x in sess.launch_log if x[0] == "wave5"]
+    gpu_launches = len(sess.launch_log)
+    kern_ms = sum(sess.elapsed_ms(a, b) for _k, _c, _d, _s, a, b in wave_launches)
+    kern_bytes = sum(12 * cells for _k, cells, *_ in wave_launches)
+    dom_launch = max(wave_launches, key=lambda x: x[1])
+    sess.recycle()
+    sess.close()
+    dev_ms = dist.max(dev_ms)
+    cells = H * Wd * steps * args.steps
+    value = 12 * cells / (dev_ms / 1e3) / 1e9
+    achieved = kern_bytes / (kern_ms / 1e3) / 1e9
+    achieved = dist.min(achieved)
+    clk = clocks.summary()
+
+    # ---- end to end through run(plan) -------------------------------------
+    gather = "root" if world == 1 else "local"
+    out_box = Box((lo, 0), (hi, Wd))
+    out = {"u": E.pinned_empty((H, Wd), np.float32, out_box),
+           "up": E.pinned_empty((H, Wd), np.float32, out_box)}
+    for _ in range(max(1, args.warmup)):
+        E.run(plan, gather=gather, out=out, trace=False)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = E.run(plan, gather=gather, out=out, trace=False)
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e = 12 * cells / e2e_s / 1e9
+    h2d = 2 * (rows[1] - rows[0]) * Wd * 4 if world > 1 else 2 * H * Wd * 4
+    h2d = int(dist.sum(h2d))
+    d2h = int(dist.sum(2 * (hi - lo) * Wd * 4))
+    newest = W.wave_result_buffer(steps)
+    field = res.buffers[newest][lo:hi]
+    finite = bool(np.isfinite(field).all())
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "wave5_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            t = json.load(fh)
+        if t.get("cells"):
+            traffic = t["dram_bytes"] / t["cells"] * dom_launch[1]
+
+    return {
+        "value": value, "ms_per_step": dev_ms / args.steps, "plan_s": plan_s,
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],
+                     "unit": "GB/s", "frac": achieved / peaks[0]["hbm_gbs"], "traffic": traffic,
+                     "kernel": "wave5_rows_kernel<float,32>", "bytes_per_cell": 12,
+                     "peak_source": peaks[1] + " hbm_gbs (torch copy)"},
+        "clocks": clk,
+        "gpu_launches": gpu_launches,
+        "H": H, "W": Wd,
+    }
+
+
+# -------------------------------------------------------- other BASELINE kernels
+
+def _timed_session(plan, placement, dist, reps, warm=2):
+    from paper_2505_06022_b200 import executor as E
+    sess = E.Session(plan, placement, trace=True)
+    sess.execute(upload=True)
+    sess.synchronize()
+    sess.recycle()
+    for _ in range(warm):
+        sess.execute(upload=False)
+        sess.synchronize()
+        sess.recycle()
+    dist.barrier()
+    m0 = sess.mark()
+    for _ in range(reps):
+        sess.execute(upload=False)
+    m1 = sess.mark()
+    sess.synchronize()
+    ms = max(sess.elapsed_ms(m0[d], m1[d]) for d in sess.devices)
+    log = list(sess.launch_log)
+    per_kind = {}
+    for kind, cells, _d, _s, a, b in log:
+        k = per_kind.setdefault(kind, [0, 0.0, 0])
+        k[0] += cells
+        k[1] += sess.elapsed_ms(a, b)
+        k[2] += 1
+    sess.recycle()
+    return sess, dist.max(ms), per_kind, len(log)
+
+
+def energy_loop(sess, seconds=1.0):
+    """J per execute over >= ``seconds`` (NVML counter deltas)."""
+    try:
+        e0 = sess.energy_mj()
+    except Exception as exc:  # noqa: BLE001
+        return {"error": str(exc)}
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds or n < 3:
+        sess.execute(upload=False)
+        n += 1
+        if n % 4 == 0:
+            sess.synchronize()
+            sess.recycle()
+    sess.synchronize()
+    sess.recycle()
+    dt = time.perf_counter() - t0
+    e1 = sess.energy_mj()
+    joules = sum(e1[d] - e0[d] for d in e0) / 1000.0
+    from paper_2505_06022_b200 import _native as N
+    import ctypes
+    cur, mx = ctypes.c_uint(), ctypes.c_uint()
+    try:
+        N.call("cq_nvml_sm_clock_mhz", sess.devices[0], ctypes.byref(cur), ctypes.byref(mx))
+        clock = cur.value
+    except Exception:  # noqa: BLE001
+        clock = None
+    return {"j_per_iter": joules / n, "watts": joules / dt, "iters": n, "seconds": dt,
+            "sm_clock_mhz": clock}
+
+
+def bench_kernels(args, dist, placement, peaks):
+    import paper_2505_06022_b200 as cq
+    from paper_2505_06022_b200 import workloads as W
+    world = dist.world
+    sm_mhz = None
+    out = {}
+    fp32_peak = lambda mhz: 148 * 128 * 2 * mhz * 1e6 / 1e12  # noqa: E731
+
+    # SAXPY: BASELINE config 0 (2^24, 4 chunks) and a beyond-L2 point 2^28
+    for n, label in ((1 << 24, "saxpy_2p24"), (1 << 28, "saxpy_2p28")):
+        prog = W.saxpy_program(n, kind="float32")
+        plan = cq.generate_commands(prog.graph(), world)
+        sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=20)
+        k = kinds.get("saxpy", [0, 1.0, 1])
+        achieved = dist.min(12 * k[0] / (k[1] / 1e3) / 1e9)
+        out[label] = {"value": 12 * n * 20 / (ms / 1e3) / 1e9, "unit": "GB/s", "scaling": "strong",
+                      "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],
+                                   "frac": achieved / peaks[0]["hbm_gbs"]},
+                      "note": "2^24 x fp32 (192 MiB) fits in L2" if n == 1 << 24 else "inputs > L2"}
+        sess.close()
+
+    # N-body: 262144 bodies, 'all' mapper all-gather each step
+    nb = args.nbody
+    prog = W.nbody_program(nb, steps=3)
+    plan = cq.generate_commands(prog.graph(), world)
+    sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=3, warm=1)
+    k = kinds.get("native", [0, 1.0, 1])
+    inter = nb * nb * 3 * 3
+    gflops = 20 * inter / (ms / 1e3) / 1e9
+    energy = energy_loop(sess, 1.0) if args.energy else None
+    clk = (energy or {}).get("sm_clock_mhz") or sm_mhz
+    out["nbody_262144"] = {"value": gflops, "unit": "GFLOP/s", "scaling": "strong",
+                           "ms_per_step": ms / 9, "flop_per_interaction": 20,
+                           "fp32_peak_tflops_at_max_clock": fp32_peak(1965),
+                           "frac_of_fp32_peak_at_max_clock": gflops / 1e3 / fp32_peak(1965),
+                           "frac_of_fp32_peak_at_observed_clock":
+                               (gflops / 1e3 / fp32_peak(clk)) if clk else None,
+                           "observed_sm_mhz": clk, "energy": energy}
+    sess.close()
+
+    # sgemm 16384^3 (slice mappers), FFMA (tcgen05 3xTF32 reported when built)
+    for variant in args.sgemm_variants:
+        m = args.sgemm
+        a = np.empty((m, m), np.float32)
+        b = np.empty((m, m), np.float32)
+        rng = np.random.default_rng(5)
+        a[...] = rng.uniform(-1, 1, (m, m)).astype(np.float32)
+        b[...] = rng.uniform(-1, 1, (m, m)).astype(np.float32)
+        prog = W.sgemm_program(m, m, m, variant=variant, a=a, b=b)
+        plan = cq.generate_commands(prog.graph(), world)
+        try:
+            sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=3, warm=1)
+        except Exception as exc:  # noqa: BLE001
+            out[f"sgemm_{variant}"] = {"error": str(exc)}
+            continue
+        tflops = 2 * m ** 3 * 3 / (ms / 1e3) / 1e12
+        out[f"sgemm_{variant}_{m}"] = {"value": tflops * 1e3, "unit": "GFLOP/s", "scaling": "strong",
+                                       "frac_of_fp32_peak_at_max_clock": tflops / fp32_peak(1965)}
+        sess.close()
+    return out
+
+
+# ------------------------------------------------------------- CPU baselines
+
+def cpu_wave_baseline(seconds=12.0, size=SIZE):
+    """The CPU port of the wave step (oracle/cq_oracle.c, OpenMP over all
+    host threads) on the same 16384^2 fp32 grid, bounded to ~``seconds``."""
+    from oracle import native as onat
+    u = np.random.default_rng(2).uniform(0, 1, (size, size)).astype(np.float32)
+    up = u.copy()
+    onat.wave_step(u, up, C, out=up)  # warm
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds:
+        if n % 2 == 0:
+            onat.wave_step(u, up, C, out=up)
+        else:
+            onat.wave_step(up, u, C, out=u)
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": 12 * size * size * n / dt / 1e9, "unit": "GB/s", "cores": os.cpu_count(),
+            "kind": "port", "sample": f"{n} wave steps of {size}x{size} fp32 "
+                                      f"(oracle/cq_oracle.c, OpenMP, {os.cpu_count()} threads)"}
+
+
+def reference_arm(args, dist):
+    """--impl reference: the reference's CPU implementation of the path on the
+    host cores.  The reference is pure Python (clusterq) and does not travel
+    to the GPU box, so this times its C restatement (oracle/), all threads."""
+    if dist.rank != 0:
+        return None
+    from oracle import native as onat
+    size = args.size
+    u = np.random.default_rng(2).uniform(0, 1, (size, size)).astype(np.float32)
+    up = u.copy()
+    for _ in range(args.warmup):
+        onat.wave_step(u, up, C, out=up)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        if s % 2 == 0:
+            onat.wave_step(u, up, C, out=up)
+        else:
+            onat.wave_step(up, u, C, out=u)
+    dt = time.perf_counter() - t0
+    val = 12 * size * size * args.steps / dt / 1e9
+    return {
+        "metric": "wave_sim 5-pt stencil effective HBM bandwidth (GB/s, 12 B/cell/step)",
+        "impl": "reference", "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"wave_sim 2-D 5-point stencil {size}x{size} fp32 per GPU, 1 time step "
+                               f"per bench step (bounded CPU sample of the 100-step run)"},
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{args.steps} wave steps of {size}x{size} fp32, "
+                                   f"oracle/cq_oracle.c OpenMP {os.cpu_count()} threads"},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--size", type=int, default=SIZE)
+    ap.add_argument("--wave-steps", type=int, default=WAVE_STEPS)
+    ap.add_argument("--nbody", type=int, default=262144)
+    ap.add_argument("--sgemm", type=int, default=16384)
+    ap.add_argument("--sgemm-variants", default="ffma")
+    ap.add_argument("--no-kernels", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-energy", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    args.sgemm_variants = [v for v in args.sgemm_variants.split(",") if v]
+    args.energy = not args.no_energy
+
+    if args.impl == "reference":
+        # rank 0 alone runs the CPU reference arm; other ranks exit at once
+        if _env_int("RANK", 0) != 0:
+            return 0
+
+        class _Rank0:
+            rank = 0
+        print(json.dumps(reference_arm(args, _Rank0())))
+        return 0
+
+    dist = Dist(args.gpus)
+    from paper_2505_06022_b200 import executor as E
+    if dist.world > 1:
+        placement = E.init_distributed(dist.rank, dist.world, dist.local_rank)
+    else:
+        placement = E.Placement(1, 0, (0,))
+    peaks = measured_peaks()
+    wave = bench_wave(args, dist, placement, peaks)
+    kernels = None if args.no_kernels else bench_kernels(args, dist, placement, peaks)
+    cpu = None
+    if dist.world == 1 and dist.rank == 0 and not args.no_cpu:
+        cpu = cpu_wave_baseline()
+    if dist.rank == 0:
+        line = {
+            "metric": "wave_sim 5-pt stencil effective HBM bandwidth (GB/s, 12 B/cell/step), "
+                      "plus per-kernel GB/s|GFLOP/s and % roofline",
+            "value": wave["value"], "unit": "GB/s", "n_gpus": dist.world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": wave["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"wave_sim 2-D 5-point stencil {args.size}x{args.size} fp32 per GPU "
+                                   f"(global {wave['H']}x{wave['W']}), {args.wave_steps} time steps per "
+                                   f"bench step, neighborhood(1,1) halo exchange",
+                       "parallelism": f"dp{dist.world} (row slabs, one rank per GPU)",
+                       "l2": "inputs 2 GiB/GPU >> 126 MB L2 (no flush needed)",
+                       "plan_s": wave["plan_s"], "init": "Gaussian pulse (SURVEY.md §8d)"},
+            "e2e": wave["e2e"], "roofline": wave["roofline"], "cpu_baseline": cpu,
+            "clocks": wave["clocks"], "gpu_launches": wave["gpu_launches"],
+            "kernels": kernels,
+        }
+        print(json.dumps(line))
+    if dist.world > 1:
+        E.shutdown_distributed()
+    dist.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

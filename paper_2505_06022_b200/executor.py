@@ -40,7 +40,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native as N
-from .errors import EvalError, MapperViolationError, ValidationError
+from .errors import EvalError, MapperViolationError, NativeError, ValidationError
 from .lowering import bind_task
 from .model import AccessMode, NativeKernel, apply_mapper
 from .region import Box, Region
@@ -185,30 +185,78 @@ def shutdown_distributed():
 
 # ---------------------------------------------------------------- host memory
 
-_pinned = {}
+_pinned = {}   # (start, end) byte span -> owning array (kept alive)
+_temp_spans = set()
+_PAGE = 4096
+# Only arrays this large are page-locked: glibc serves them from their own
+# mmap'd pages, so a registration never shares a page with another array.
+PIN_MIN_BYTES = 64 << 20
+
+
+def _byte_span(arr, box):
+    if box is None:
+        return arr.ctypes.data, arr.ctypes.data + arr.nbytes
+    lo = sum(m * s for m, s in zip(box.mins, arr.strides))
+    hi = sum((m - 1) * s for m, s in zip(box.maxs, arr.strides)) + arr.itemsize
+    return arr.ctypes.data + lo, arr.ctypes.data + hi
+
+
+def _pin_state(start, end):
+    """"pinned" (inside one registration), "partial" (overlaps one -- a DMA
+    over it would be invalid) or "free" (pageable, no registration)."""
+    for s, e in list(_pinned) + list(_temp_spans):
+        if s <= start and end <= e:
+            return "pinned"
+        if s < end and start < e:
+            return "partial"
+    return "free"
+
+
+def _pin_span(arr: np.ndarray, box=None, keep=True):
+    """Page-lock the bytes of a large ``arr`` spanning ``box`` (whole array if
+    None); a rank of a weak-scaled run pins only its own rows of a big host
+    array.  Returns the span when registered temporarily (keep=False)."""
+    if arr.nbytes < PIN_MIN_BYTES:
+        return None
+    a, b = _byte_span(arr, box)
+    start = a // _PAGE * _PAGE
+    end = -(-b // _PAGE) * _PAGE
+    if _pin_state(start, end) != "free":
+        return None
+    N.call("cq_host_register", ctypes.c_void_p(start), end - start)
+    if keep:
+        _pinned[(start, end)] = arr
+        return None
+    _temp_spans.add((start, end))
+    return (start, end)
+
+
+def _needs_bounce(arr, box):
+    """True when a DMA over ``box`` of ``arr`` would straddle a registration
+    edge; such copies go through a temporary pageable array instead."""
+    return _pin_state(*_byte_span(arr, box)) == "partial"
+
+
+def _unpin_temp(span):
+    N.call("cq_host_unregister", ctypes.c_void_p(span[0]))
+    _temp_spans.discard(span)
 
 
 def _pin(arr: np.ndarray):
-    """Page-lock a host array once (cached by address) for async DMA."""
-    if arr.nbytes < (1 << 20):
-        return
-    key = (arr.ctypes.data, arr.nbytes)
-    if key in _pinned:
-        return
-    N.call("cq_host_register", ctypes.c_void_p(arr.ctypes.data), arr.nbytes)
-    _pinned[key] = arr  # keep alive while registered
+    _pin_span(arr, None, keep=True)
 
 
 def release_pinned():
-    for (ptr, _n), _a in list(_pinned.items()):
-        N.call("cq_host_unregister", ctypes.c_void_p(ptr))
+    for (start, _end), _a in list(_pinned.items()):
+        N.call("cq_host_unregister", ctypes.c_void_p(start))
     _pinned.clear()
 
 
-def pinned_empty(shape, dtype) -> np.ndarray:
-    """A page-locked host array (for inputs / outputs of repeated runs)."""
+def pinned_empty(shape, dtype, box=None) -> np.ndarray:
+    """A host array page-locked over ``box`` (whole array if None) for the
+    inputs / outputs of repeated runs."""
     arr = np.empty(shape, dtype=dtype)
-    _pin(arr)
+    _pin_span(arr, box, keep=True)
     return arr
 
 
@@ -334,15 +382,17 @@ def kahn_order(plan: Plan) -> list:
     return order
 
 
-class _Run:
-    def __init__(self, plan: Plan, placement: Placement, gather: str, out: Optional[dict],
-                 trace: bool, energy: bool):
+class Session:
+    """A plan bound to this process's GPUs: allocations persist across
+    ``execute`` calls, so a program can be re-run on device-resident data.
+
+    ``run()`` is one upload + execute + gather; benchmarks use the pieces."""
+
+    def __init__(self, plan: Plan, placement: Optional[Placement] = None, trace: bool = True):
+        placement = placement or local_placement()
         self.plan = plan
         self.pl = placement
-        self.gather = gather
-        self.out_arrays = out or {}
         self.want_trace = trace
-        self.want_energy = energy
         self.buffers = plan.graph.buffers
         self.by_id = {c.id: c for c in plan.commands}
         self.nodes = plan.node_count
@@ -354,8 +404,33 @@ class _Run:
         self.free_events = {}
         self.haz = _Hazards()
         self.bindings = {}
-        self.trace_marks = []   # (cmd, kind, node, device, [(ev0, ev1)], bytes)
+        self.trace_marks = []   # per command: timing events for the trace
+        self.launch_log = []    # (binding kind, cells, device, start, stop) per kernel launch
         self.host_init = {}
+        self._sched = None
+        self.t0 = None
+        self._t0 = {}
+        self.uploading = True
+        self.bounce = []        # temporaries of bounced host copies (kept until sync)
+        for d in self.devices:
+            N.call("cq_init_device", d)
+        kahn_order(plan)  # validates acyclicity before touching devices
+        self.allocate()
+        self.pin_inputs()
+
+    def pin_inputs(self):
+        """Page-lock, once per process, the span of each host input array
+        that this process uploads (node 0's copy and version-1 destinations)."""
+        need = {}
+        for (node, buf), view in self.views.items():
+            if node == 0 and self.buffers[buf].init.kind in ("array", "values"):
+                need.setdefault(buf, []).append(view.box)
+        for c in self.plan.commands:
+            if isinstance(c, PushCommand) and not c.deps and self.local(c.dst) \
+                    and self.buffers[c.buffer].init.kind in ("array", "values"):
+                need.setdefault(c.buffer, []).append(c.region.bounding_box())
+        for buf, boxes in need.items():
+            _pin_span(self.host_array(buf), _bbox_union(boxes), keep=True)
 
     # ---- small helpers -------------------------------------------------
     def dev(self, node):
@@ -425,10 +500,7 @@ class _Run:
         arr = self.host_init.get(buf)
         if arr is None:
             b = self.buffers[buf]
-            arr = b.init.materialize(b.extent, b.element_kind)
-            if b.init.kind in ("array", "values"):
-                arr = np.ascontiguousarray(arr)
-                _pin(arr)
+            arr = np.ascontiguousarray(b.init.materialize(b.extent, b.element_kind))
             self.host_init[buf] = arr
         return arr
 
@@ -446,6 +518,13 @@ class _Run:
                 cb = _cbox(box)
                 if init.kind in ("array", "values"):
                     arr = self.host_array(buf)
+                    if _needs_bounce(arr, box):
+                        sl = tuple(slice(lo, hi) for lo, hi in zip(box.mins, box.maxs))
+                        tmp = np.ascontiguousarray(arr[sl])
+                        self.bounce.append(tmp)
+                        N.call("cq_copy_box_h2d", dev, stream, b.itemsize, ctypes.byref(view.c),
+                               ctypes.c_void_p(tmp.ctypes.data), ctypes.byref(cb), ctypes.byref(cb))
+                        continue
                     N.call("cq_copy_box_h2d", dev, stream, b.itemsize, ctypes.byref(view.c),
                            ctypes.c_void_p(arr.ctypes.data), ctypes.byref(ext), ctypes.byref(cb))
                 else:
@@ -476,7 +555,7 @@ class _Run:
             src_l, dst_l = self.local(push.src), self.local(push.dst)
             if not push.deps:
                 # host-initialised data: the destination materialises it
-                if dst_l:
+                if dst_l and self.uploading:
                     t = self.materialize(push.dst, push.buffer, push.region, N.STREAM_COMM)
                     self.mark_transfer(push, push.dst, t)
                 continue
@@ -572,7 +651,7 @@ class _Run:
             self.trace_marks.append((push, node, self.dev(node), start, stop))
 
     # ---- executes --------------------------------------------------------
-    def execute(self, cmd: ExecuteCommand, awaited):
+    def exec_command(self, cmd: ExecuteCommand, awaited):
         task = self.plan.graph.task(cmd.task_id)
         binding = self.bindings.get(task.id)
         if binding is None:
@@ -615,9 +694,12 @@ class _Run:
                     acc.append((node, a.buffer, reg, False))
             for a in task.writes():
                 acc.append((node, a.buffer, Region.from_box(box), True))
-            marks.append(self.issue(dev, stream, acc,
-                                    lambda box=box, stream=stream: self.launch(
-                                        binding, task, cmd, box, dev, stream, rviews, wviews, reads)))
+            t = self.issue(dev, stream, acc,
+                           lambda box=box, stream=stream: self.launch(
+                               binding, task, cmd, box, dev, stream, rviews, wviews, reads))
+            marks.append(t)
+            if self.want_trace:
+                self.launch_log.append((binding.kind, box.volume(), dev, stream, t[0], t[1]))
         if self.want_trace:
             self.trace_marks.append((cmd, node, dev, marks, None))
 
@@ -802,72 +884,122 @@ class _Run:
         N.call("cq_expr_eval", dev, stream, ctypes.byref(X))
 
     # ---- the walk --------------------------------------------------------
-    def run(self):
-        order = kahn_order(self.plan)
-        for d in self.devices:
-            N.call("cq_init_device", d)
-        e0 = {}
-        energy0 = {}
-        if self.want_energy:
-            for d in self.devices:
-                try:
-                    mj = ctypes.c_uint64()
-                    N.call("cq_nvml_energy_mj", d, ctypes.byref(mj))
-                    energy0[d] = mj.value
-                except Exception:
-                    energy0 = {}
-                    break
-        self.allocate()
-        for d in self.devices:
-            ev = self.event(d, timing=True)
-            N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
-            e0[d] = ev
-            for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
-                N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
-        self.seed_node0()
-
-        group = []
-        group_acc = []
-        awaited_by_exec = {}
-        pending_await = {}
-        for cid in order:
+    def schedule(self):
+        """Global transfer groups and per-execute awaited regions (identical
+        on every rank; computed once per session)."""
+        if self._sched is not None:
+            return self._sched
+        steps = []   # ("group", [push...]) | ("exec", cmd, awaited)
+        group, group_acc = [], []
+        for cid in kahn_order(self.plan):
             c = self.by_id[cid]
             if isinstance(c, ExecuteCommand):
-                self.flush_group(group)
+                if group:
+                    steps.append(("group", group))
                 group, group_acc = [], []
-                if self.local(c.node):
-                    aw = {}
-                    for d in c.deps:
-                        a = self.by_id[d]
-                        if isinstance(a, AwaitPushCommand) and a.dst == c.node:
-                            aw[a.buffer] = aw[a.buffer].union(a.region) if a.buffer in aw else a.region
-                    self.execute(c, aw)
+                aw = {}
+                for d in c.deps:
+                    a = self.by_id[d]
+                    if isinstance(a, AwaitPushCommand) and a.dst == c.node:
+                        aw[a.buffer] = aw[a.buffer].union(a.region) if a.buffer in aw else a.region
+                steps.append(("exec", c, aw))
             elif isinstance(c, PushCommand):
                 acc = [(c.src, c.buffer, c.region, False), (c.dst, c.buffer, c.region, True)]
                 if any(n == n2 and b == b2 and (w or w2) and r.overlaps(r2)
                        for n, b, r, w in acc for n2, b2, r2, w2 in group_acc):
-                    self.flush_group(group)
+                    steps.append(("group", group))
                     group, group_acc = [], []
                 group.append(c)
                 group_acc.extend(acc)
-            # AwaitPush: its receive was posted with the push (same group)
-        self.flush_group(group)
+            # AwaitPush: its receive is posted with the push (same group)
+        if group:
+            steps.append(("group", group))
+        self._sched = steps
+        return steps
 
+    def execute(self, upload: bool = True):
+        """Issue every local command of the plan (asynchronous).
+
+        upload=True materialises host-initialised data first (node 0's copy
+        and the destinations of version-1 pushes); upload=False re-runs the
+        commands on the device-resident state (benchmarking)."""
+        if self.t0 is None:
+            for d in self.devices:
+                ev = self.event(d, timing=True)
+                N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
+                self._t0[d] = ev
+                for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
+                    N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
+            self.t0 = dict(self._t0)
+        self.uploading = upload
+        if upload:
+            self.seed_node0()
+        for step in self.schedule():
+            if step[0] == "group":
+                self.flush_group(step[1])
+            elif self.local(step[1].node):
+                self.exec_command(step[1], step[2])
+
+    def mark(self):
+        """Join all streams of every local device and record a timing event
+        per device on the compute stream; returns {device: event}."""
+        out = {}
+        for d in self.devices:
+            for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
+                ev = self.event(d)
+                N.call("cq_event_record", ctypes.c_uint64(ev), d, s)
+                N.call("cq_stream_wait_event", d, N.STREAM_COMPUTE, ctypes.c_uint64(ev))
+            ev = self.event(d, timing=True)
+            N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
+            for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
+                N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
+            out[d] = ev
+        return out
+
+    @staticmethod
+    def elapsed_ms(a, b):
+        ms = ctypes.c_float()
+        N.call("cq_event_elapsed_ms", ctypes.c_uint64(a), ctypes.c_uint64(b), ctypes.byref(ms))
+        return ms.value
+
+    def synchronize(self):
         for d in self.devices:
             for s in (N.STREAM_COMPUTE, N.STREAM_BOUNDARY, N.STREAM_COMM):
                 N.call("cq_stream_synchronize", d, s)
+        self.bounce.clear()
         self.check_errors()
-        result = self.collect()
-        measured = {}
-        if energy0:
-            for d in self.devices:
-                mj = ctypes.c_uint64()
-                N.call("cq_nvml_energy_mj", d, ctypes.byref(mj))
-                measured[f"energy_j_device{d}"] = (mj.value - energy0[d]) / 1000.0
-        trace, makespan = self.build_trace(e0)
+
+    def energy_mj(self):
+        out = {}
+        for d in self.devices:
+            mj = ctypes.c_uint64()
+            N.call("cq_nvml_energy_mj", d, ctypes.byref(mj))
+            out[d] = mj.value
+        return out
+
+    def recycle(self):
+        """After a synchronize: forget hazards, recycle events and traces."""
+        self.haz = _Hazards()
+        for dev, timing, ev in self.events:
+            self.free_events.setdefault((dev, timing), []).append(ev)
+        self.events = []
+        self.trace_marks = []
+        self.launch_log = []
+        self.t0 = None
+        self._t0 = {}
+
+    def close(self):
         self.release()
-        return RunResult(buffers=result, trace=trace, makespan=makespan, plan=self.plan,
-                         measured=measured)
+        for pool in self.free_events.values():
+            for ev in pool:
+                N.call("cq_event_destroy", ctypes.c_uint64(ev))
+        self.free_events = {}
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
     def check_errors(self):
         for d in self.devices:
@@ -880,22 +1012,32 @@ class _Run:
                 raise MapperViolationError(f"read at id {tuple(pt)} outside the mapped region")
 
     # ---- gather ------------------------------------------------------------
-    def collect(self):
-        if self.gather == "none":
+    def results(self, gather: str = "root", out: Optional[dict] = None):
+        """Final buffers: each final piece from its lowest-id holder
+        (simulator.py:210-222).  Call after ``synchronize``."""
+        self.gather = gather
+        out_arrays = out or {}
+        if gather == "none":
             return {}
         out = {}
         root = self.pl.rank == 0
         pending = []
         for name, entries in self.plan.final_locations.items():
             b = self.buffers[name]
-            arr = self.out_arrays.get(name)
+            arr = out_arrays.get(name)
+            covered = sum(r.volume() for r, _v, _h in entries) == b.extent.volume()
             if arr is None:
                 arr = np.zeros(b.extent.shape, dtype=b.dtype)
-            else:
+            elif not covered:
                 arr[...] = 0
             init_v1 = b.init.is_initialized
             for region, version, holders in entries:
                 src = min(holders)
+                if gather == "local":
+                    # every piece this rank holds a copy of (lowest local holder)
+                    mine = [h for h in holders if self.local(h)]
+                    if mine:
+                        src = min(mine)
                 if init_v1 and version == 1:
                     if root or self.gather == "local":
                         host = self.host_array(name)
@@ -911,30 +1053,50 @@ class _Run:
             out[name] = arr
         direct = [p for p in pending if p[0] != "nccl"]
         temp_pins = []
+        # page-lock fresh result arrays only for the copies (the caller owns
+        # them afterwards), one span per array covering all its pieces;
+        # `out=` arrays from pinned_empty stay pinned
+        spans = {}
         for view, arr, region in direct:
-            key = (arr.ctypes.data, arr.nbytes)
-            if arr.nbytes >= (1 << 20) and key not in _pinned and key not in temp_pins:
-                # page-lock fresh result arrays only for the copy (the caller
-                # owns them afterwards); `out=` arrays from pinned_empty stay pinned
-                N.call("cq_host_register", ctypes.c_void_p(arr.ctypes.data), arr.nbytes)
-                temp_pins.append(key)
+            bb = region.bounding_box()
+            key = id(arr)
+            prev = spans.get(key)
+            spans[key] = (arr, bb if prev is None else Box(
+                [min(a, b) for a, b in zip(prev[1].mins, bb.mins)],
+                [max(a, b) for a, b in zip(prev[1].maxs, bb.maxs)]))
+        for arr, bb in spans.values():
+            span = _pin_span(arr, bb, keep=False)
+            if span is not None:
+                temp_pins.append(span)
+        bounced = []
+        for view, arr, region in direct:
             ha = N.box3((0,) * arr.ndim, arr.shape)
             for box in region.boxes:
+                cb = _cbox(box)
+                if _needs_bounce(arr, box):
+                    tmp = np.empty(box.shape, dtype=arr.dtype)
+                    bounced.append((arr, box, tmp))
+                    N.call("cq_copy_box_d2h", view.device, N.STREAM_COMM, view.itemsize,
+                           ctypes.c_void_p(tmp.ctypes.data), ctypes.byref(cb), ctypes.byref(view.c),
+                           ctypes.byref(cb))
+                    continue
                 N.call("cq_copy_box_d2h", view.device, N.STREAM_COMM, view.itemsize,
                        ctypes.c_void_p(arr.ctypes.data), ctypes.byref(ha), ctypes.byref(view.c),
-                       ctypes.byref(_cbox(box)))
+                       ctypes.byref(cb))
         remote = [p for p in pending if p[0] == "nccl"]
         if remote:
-            self.gather_remote(remote)
+            self.gather_remote(remote, bounced)
         for d in self.devices:
             N.call("cq_stream_synchronize", d, N.STREAM_COMM)
-        for ptr, _n in temp_pins:
-            N.call("cq_host_unregister", ctypes.c_void_p(ptr))
+        for arr, box, tmp in bounced:
+            arr[tuple(slice(lo, hi) for lo, hi in zip(box.mins, box.maxs))] = tmp
+        for span in temp_pins:
+            _unpin_temp(span)
         if self.gather == "root" and not root:
             return {}
         return out
 
-    def gather_remote(self, items):
+    def gather_remote(self, items, bounced):
         """Ship final pieces held by other ranks to rank 0 over NCCL."""
         dev = self.pl.devices[0]
         ops = []
@@ -961,7 +1123,6 @@ class _Run:
             N.call(fn, dev, N.STREAM_COMM, ctypes.c_void_p(ptr), nbytes, peer)
         N.call("cq_nccl_group_end")
         for ptr, arr, box, eb in unpack:
-            _pin(arr)
             ha = N.box3((0,) * arr.ndim, arr.shape)
             dense = N.CqView()
             dense.ptr = ptr
@@ -970,13 +1131,23 @@ class _Run:
             dense.alloc.hi[:] = hi
             sh = [h - l for l, h in zip(lo, hi)]
             dense.stride[:] = [sh[1] * sh[2], sh[2], 1]
+            cb = _cbox(box)
+            if _needs_bounce(arr, box):
+                tmp = np.empty(box.shape, dtype=arr.dtype)
+                bounced.append((arr, box, tmp))
+                N.call("cq_copy_box_d2h", dev, N.STREAM_COMM, eb, ctypes.c_void_p(tmp.ctypes.data),
+                       ctypes.byref(cb), ctypes.byref(dense), ctypes.byref(cb))
+                continue
             N.call("cq_copy_box_d2h", dev, N.STREAM_COMM, eb, ctypes.c_void_p(arr.ctypes.data),
-                   ctypes.byref(ha), ctypes.byref(dense), ctypes.byref(_cbox(box)))
+                   ctypes.byref(ha), ctypes.byref(dense), ctypes.byref(cb))
 
     # ---- trace -------------------------------------------------------------
-    def build_trace(self, e0):
+    def trace(self):
+        """(trace events, makespan) of the commands issued since the last
+        ``recycle``; times in seconds from the first ``execute``."""
         trace = []
-        if not self.want_trace:
+        e0 = self.t0
+        if not self.want_trace or not e0:
             return trace, Fraction(0)
 
         def secs(dev, ev):
@@ -1066,5 +1237,23 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
         raise ValidationError("link must be a LinkModel")
     if gather not in ("root", "local", "none"):
         raise ValidationError(f"unknown gather mode '{gather}'")
-    pl = placement or local_placement()
-    return _Run(plan, pl, gather, out, trace, energy).run()
+    session = Session(plan, placement, trace)
+    try:
+        e_before = None
+        if energy:
+            try:
+                e_before = session.energy_mj()
+            except NativeError:
+                e_before = None
+        session.execute(upload=True)
+        session.synchronize()
+        buffers = session.results(gather, out)
+        measured = {}
+        if e_before is not None:
+            e_after = session.energy_mj()
+            for d in session.devices:
+                measured[f"energy_j_device{d}"] = (e_after[d] - e_before[d]) / 1000.0
+        events, makespan = session.trace()
+    finally:
+        session.close()
+    return RunResult(buffers=buffers, trace=events, makespan=makespan, plan=plan, measured=measured)

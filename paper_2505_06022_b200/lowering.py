@@ -18,10 +18,15 @@ results -- tests/test_gpu_parity.py cross-checks fast paths against the
 interpreter.
 """
 
+import os
 from dataclasses import dataclass, field
 
 from . import kernel as K
 from .model import AccessMode, NativeKernel, collect_read_offsets
+
+# Specialised kernels for recognised bodies; tests switch this off to check
+# that the interpreter and the fast paths agree bit for bit.
+FAST_PATHS = os.environ.get("CQ_FAST_PATHS", "1") == "1"
 
 
 @dataclass
@@ -109,7 +114,7 @@ def bind_task(task, buffers) -> Binding:
                      if accs[name].buffer in written and any(any(o) for o in offs))
 
     writes = task.writes()
-    if len(writes) == 1 and not snap:
+    if FAST_PATHS and len(writes) == 1 and not snap:
         w = writes[0]
         kind = buffers[w.buffer].element_kind
         expr = task.body[w.name]

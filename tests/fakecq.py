@@ -1,0 +1,408 @@
+"""A numpy test double of libcq (include/cq.h) for CPU-only tests.
+
+TEST INFRASTRUCTURE ONLY.  It lets the executor's host logic -- allocation,
+Kahn-order walk, transfer grouping, NCCL send/recv matching, hazard events,
+interior/boundary splitting, snapshots, the packed CqExpr struct, gather --
+run without a GPU, including a 2-rank torch.distributed *gloo* run where
+the NCCL group ops travel over gloo.  Kernels are plain numpy with the same
+per-operator rounding; the real kernels are tested on the B200 by
+tests/test_gpu_parity.py.  Installed by monkeypatching ``_native._lib``.
+"""
+
+import ctypes
+
+import numpy as np
+
+from paper_2505_06022_b200 import _native as N
+
+_DT = {N.CQ_F64: np.float64, N.CQ_F32: np.float32, N.CQ_I64: np.int64}
+
+
+def _val(x):
+    return x.value if hasattr(x, "value") else x
+
+
+def _obj(x):
+    return x._obj if hasattr(x, "_obj") else x
+
+
+class FakeLib:
+    def __init__(self, ndev=1, transport=None):
+        self.ndev = ndev
+        self.blocks = {}      # base -> np.uint8 array
+        self.next = 1 << 44
+        self.err = b""
+        self.transport = transport
+        self.group = None
+        self.flag = None
+        self.launches = []
+        self.events = 0
+
+    # ----------------------------------------------------------- memory
+    def _mem(self, addr, nbytes):
+        for base, blk in self.blocks.items():
+            if base <= addr < base + blk.size:
+                off = addr - base
+                assert off + nbytes <= blk.size, "device access out of bounds"
+                return blk[off:off + nbytes]
+        buf = (ctypes.c_uint8 * nbytes).from_address(addr)
+        return np.ctypeslib.as_array(buf)
+
+    def _arr(self, addr, shape, strides_elems, dtype):
+        dtype = np.dtype(dtype)
+        n = 1 + sum((s - 1) * st for s, st in zip(shape, strides_elems)) if all(shape) else 0
+        raw = self._mem(addr, n * dtype.itemsize)
+        flat = raw.view(dtype)
+        return np.lib.stride_tricks.as_strided(flat, shape=shape,
+                                               strides=[s * dtype.itemsize for s in strides_elems])
+
+    def _view(self, v, dtype, box=None):
+        """ndarray over the cells of ``box`` (global coords) of view ``v``."""
+        lo = list(v.alloc.lo)
+        box = box or v.alloc
+        off = sum((box.lo[k] - lo[k]) * v.stride[k] for k in range(3))
+        shape = [box.hi[k] - box.lo[k] for k in range(3)]
+        dt = np.dtype(dtype)
+        return self._arr(v.ptr + off * dt.itemsize, shape, list(v.stride), dt)
+
+    def _host(self, addr, alloc, box, dtype):
+        sh = [alloc.hi[k] - alloc.lo[k] for k in range(3)]
+        st = [sh[1] * sh[2], sh[2], 1]
+        off = sum((box.lo[k] - alloc.lo[k]) * st[k] for k in range(3))
+        dt = np.dtype(dtype)
+        return self._arr(addr + off * dt.itemsize, [box.hi[k] - box.lo[k] for k in range(3)], st, dt)
+
+    @staticmethod
+    def _eb(eb):
+        return {4: np.uint32, 8: np.uint64, 1: np.uint8, 2: np.uint16}[eb]
+
+    # ----------------------------------------------------------- runtime
+    def cq_last_error(self):
+        return self.err
+
+    def cq_version(self, p):
+        _obj(p).value = 1
+        return 0
+
+    def cq_device_count(self, p):
+        _obj(p).value = self.ndev
+        return 0
+
+    def cq_init_device(self, d):
+        return 0
+
+    def cq_device_props(self, d, sm, l2, clk, mem):
+        _obj(sm).value, _obj(l2).value, _obj(clk).value, _obj(mem).value = 148, 126 << 20, 1965000, 180 << 30
+        return 0
+
+    def cq_enable_peer(self, d, p, en):
+        _obj(en).value = 1
+        return 0
+
+    def cq_shutdown(self):
+        return 0
+
+    def cq_malloc(self, d, nbytes, p):
+        n = int(_val(nbytes))
+        base = self.next
+        self.next += ((n + (1 << 20)) >> 20 << 20) + (1 << 20)
+        self.blocks[base] = np.zeros(max(n, 1), np.uint8)
+        _obj(p).value = base
+        return 0
+
+    def cq_free(self, d, p):
+        self.blocks.pop(_val(p), None)
+        return 0
+
+    def cq_pool_trim(self, d):
+        return 0
+
+    def cq_host_register(self, p, n):
+        return 0
+
+    def cq_host_unregister(self, p):
+        return 0
+
+    def cq_copy_h2d(self, d, s, dst, src, n):
+        n = int(_val(n))
+        self._mem(_val(dst), n)[:] = self._mem(_val(src), n)
+        return 0
+
+    cq_copy_d2h = cq_copy_h2d
+
+    def cq_copy_box(self, d, s, eb, dst, dd, src, sd, box):
+        dt = self._eb(eb)
+        b = _obj(box)
+        self._view(_obj(dst), dt, b)[...] = self._view(_obj(src), dt, b)
+        return 0
+
+    def cq_copy_box_h2d(self, d, s, eb, dst, host, halloc, box):
+        dt = self._eb(eb)
+        b = _obj(box)
+        self._view(_obj(dst), dt, b)[...] = self._host(_val(host), _obj(halloc), b, dt)
+        return 0
+
+    def cq_copy_box_d2h(self, d, s, eb, host, halloc, src, box):
+        dt = self._eb(eb)
+        b = _obj(box)
+        self._host(_val(host), _obj(halloc), b, dt)[...] = self._view(_obj(src), dt, b)
+        return 0
+
+    def cq_pack_box(self, d, s, eb, dense, src, box):
+        dt = self._eb(eb)
+        b = _obj(box)
+        self._host(_val(dense), b, b, dt)[...] = self._view(_obj(src), dt, b)
+        return 0
+
+    def cq_unpack_box(self, d, s, eb, dst, dense, box):
+        dt = self._eb(eb)
+        b = _obj(box)
+        self._view(_obj(dst), dt, b)[...] = self._host(_val(dense), b, b, dt)
+        return 0
+
+    def cq_event_create(self, d, timing, p):
+        self.events += 1
+        _obj(p).value = self.events
+        return 0
+
+    def cq_event_destroy(self, e):
+        return 0
+
+    def cq_event_record(self, e, d, s):
+        return 0
+
+    def cq_stream_wait_event(self, d, s, e):
+        return 0
+
+    def cq_event_synchronize(self, e):
+        return 0
+
+    def cq_event_elapsed_ms(self, a, b, p):
+        _obj(p).value = 0.001 * (_val(b) - _val(a))
+        return 0
+
+    def cq_stream_synchronize(self, d, s):
+        return 0
+
+    def cq_device_synchronize(self, d):
+        return 0
+
+    # -------------------------------------------------------------- NCCL
+    def cq_nccl_unique_id(self, buf):
+        return 0
+
+    def cq_nccl_init(self, d, n, r, uid):
+        return 0
+
+    def cq_nccl_group_start(self):
+        self.group = []
+        return 0
+
+    def cq_nccl_group_end(self):
+        ops, self.group = self.group, None
+        self.transport.exchange(ops, self)
+        return 0
+
+    def cq_nccl_send(self, d, s, buf, n, peer):
+        self.group.append(("send", _val(buf), int(_val(n)), int(_val(peer))))
+        return 0
+
+    def cq_nccl_recv(self, d, s, buf, n, peer):
+        self.group.append(("recv", _val(buf), int(_val(n)), int(_val(peer))))
+        return 0
+
+    def cq_nccl_allgather(self, *a):
+        return N.CQ_ERR_UNSUPPORTED
+
+    def cq_nccl_allreduce_max_f64(self, *a):
+        return N.CQ_ERR_UNSUPPORTED
+
+    def cq_nccl_destroy(self):
+        return 0
+
+    # ----------------------------------------------------------- kernels
+    def cq_fill(self, d, s, kind, dst, box, ext, mode, val, ival):
+        dt = _DT[kind]
+        b, e = _obj(box), _obj(ext)
+        out = self._view(_obj(dst), dt, b)
+        if mode == 1:
+            e1, e2 = e.hi[1] - e.lo[1], e.hi[2] - e.lo[2]
+            i0, i1, i2 = np.meshgrid(*[np.arange(b.lo[k], b.hi[k]) for k in range(3)], indexing="ij")
+            out[...] = ((i0 * e1 + i1) * e2 + i2).astype(dt)
+        elif mode == 2:
+            out[...] = ival if kind == N.CQ_I64 else dt(_val(val))
+        else:
+            out[...] = 0
+        return 0
+
+    def cq_saxpy(self, d, s, kind, alpha, ialpha, x, y, z, n):
+        dt = _DT[kind]
+        n = int(_val(n))
+        xa = self._arr(_val(x), [n], [1], dt)
+        ya = self._arr(_val(y), [n], [1], dt)
+        za = self._arr(_val(z), [n], [1], dt)
+        a = np.int64(ialpha) if kind == N.CQ_I64 else dt(_val(alpha))
+        with np.errstate(all="ignore"):
+            za[...] = (a * xa).astype(dt) + ya
+        self.launches.append("saxpy")
+        return 0
+
+    def cq_wave5(self, d, s, kind, u, upr, out, box, ext, c, k2, k4):
+        dt = _DT[kind]
+        u, upr, out, b, e = (_obj(x) for x in (u, upr, out, box, ext))
+        H, W = e.hi[1], e.hi[2]
+        rows = np.arange(b.lo[1], b.hi[1])
+        cols = np.arange(b.lo[2], b.hi[2])
+        uu = self._view(u, dt)
+        lo1, lo2 = u.alloc.lo[1], u.alloc.lo[2]
+
+        def at(r, cc):
+            return uu[0][np.clip(r, 0, H - 1)[:, None] - lo1, np.clip(cc, 0, W - 1)[None, :] - lo2]
+        cc = at(rows, cols)
+        c, k2, k4 = dt(_val(c)), dt(_val(k2)), dt(_val(k4))
+        lap = (((at(rows - 1, cols) + at(rows + 1, cols)) + at(rows, cols - 1)) + at(rows, cols + 1)) - k4 * cc
+        res = ((k2 * cc) - self._view(upr, dt, b)[0]) + c * lap
+        self._view(out, dt, b)[0][...] = res
+        self.launches.append("wave5")
+        return 0
+
+    def cq_expr_eval(self, d, s, X):
+        X = _obj(X)
+        dt = _DT[X.kind]
+        b = X.box
+        p = np.meshgrid(*[np.arange(b.lo[k], b.hi[k], dtype=np.int64) for k in range(3)], indexing="ij")
+        shape = p[0].shape
+        results = []
+        for o in range(X.n_out):
+            stack = []
+            for pc in range(X.out_code_begin[o], X.out_code_end[o]):
+                op, arg = X.code_op[pc], X.code_arg[pc]
+                if op == 0:
+                    bits = np.int64(X.consts[arg])
+                    v = bits if X.kind == N.CQ_I64 else bits.view(np.float64)
+                    stack.append(np.full(shape, v).astype(dt))
+                elif op == 1:
+                    stack.append(p[arg].astype(dt))
+                elif op == 2:
+                    vi = X.slot_view[arg]
+                    bd = X.view_dims[vi]
+                    ext = X.view_extent[vi]
+                    q = [np.zeros(shape, np.int64) for _ in range(3)]
+                    for j in range(bd):
+                        ax = 3 - bd + j
+                        q[ax] = np.clip(p[3 - X.dims + j] + X.slot_off[arg][j], ext.lo[ax], ext.hi[ax] - 1)
+                    if X.view_n_check[vi] > 0:
+                        inside = np.zeros(shape, bool)
+                        for bi in range(X.view_n_check[vi]):
+                            cb = X.view_check[vi][bi]
+                            inside |= np.all([(q[k] >= cb.lo[k]) & (q[k] < cb.hi[k]) for k in range(3)], axis=0)
+                        if not inside.all():
+                            self.flag = N.CQ_ERR_MAPPER
+                            return 0
+                    v = X.views[vi]
+                    arr = self._view(v, dt)
+                    stack.append(arr[q[0] - v.alloc.lo[0], q[1] - v.alloc.lo[1], q[2] - v.alloc.lo[2]])
+                elif op == 3:
+                    with np.errstate(all="ignore"):
+                        stack[-1] = (-stack[-1]).astype(dt)
+                else:
+                    bb = stack.pop()
+                    aa = stack.pop()
+                    with np.errstate(all="ignore"):
+                        if op == 4:
+                            r = aa + bb
+                        elif op == 5:
+                            r = aa - bb
+                        elif op == 6:
+                            r = aa * bb
+                        elif X.kind == N.CQ_I64:
+                            if np.any(bb == 0):
+                                self.flag = N.CQ_ERR_EVAL
+                                return 0
+                            q = np.abs(aa.astype(np.float64)) // np.abs(bb.astype(np.float64))
+                            r = np.where((aa < 0) != (bb < 0), -q, q).astype(np.int64)
+                        else:
+                            r = aa / bb
+                    stack.append(r.astype(dt))
+            results.append(stack[0])
+        for o in range(X.n_out):
+            self._view(X.out[o], dt, b)[...] = results[o]
+        self.launches.append("expr")
+        return 0
+
+    def cq_error_flag(self, d, code, pt, clear):
+        _obj(code).value = self.flag or 0
+        if clear:
+            self.flag = None
+        return 0
+
+    def cq_nbody_kick(self, d, s, pos, n, vin, vout, lo, hi, eps2, dt_):
+        n, lo, hi = int(_val(n)), int(_val(lo)), int(_val(hi))
+        P = self._arr(_val(pos), [n, 4], [4, 1], np.float32).astype(np.float64)
+        vi = self._arr(_val(vin), [hi - lo, 4], [4, 1], np.float32)
+        vo = self._arr(_val(vout), [hi - lo, 4], [4, 1], np.float32)
+        d3 = P[None, :, :3] - P[lo:hi, None, :3]
+        r2 = (d3 ** 2).sum(-1) + _val(eps2)
+        a = (d3 * (P[None, :, 3] / r2 ** 1.5)[..., None]).sum(1)
+        res = vi.copy()
+        res[:, :3] += (_val(dt_) * a).astype(np.float32)
+        vo[...] = res
+        return 0
+
+    def cq_nbody_drift(self, d, s, pin, v, pout, count, dt_):
+        count = int(_val(count))
+        a = self._arr(_val(pin), [count, 4], [4, 1], np.float32).copy()
+        b = self._arr(_val(v), [count, 4], [4, 1], np.float32)
+        a[:, :3] += np.float32(_val(dt_)) * b[:, :3]
+        self._arr(_val(pout), [count, 4], [4, 1], np.float32)[...] = a
+        return 0
+
+    def cq_sgemm(self, d, s, variant, a, lda, b, ldb, c, ldc, m, n, k):
+        m, n, k = int(_val(m)), int(_val(n)), int(_val(k))
+        A = self._arr(_val(a), [m, k], [int(_val(lda)), 1], np.float32)
+        B = self._arr(_val(b), [k, n], [int(_val(ldb)), 1], np.float32)
+        self._arr(_val(c), [m, n], [int(_val(ldc)), 1], np.float32)[...] = \
+            (A.astype(np.float64) @ B.astype(np.float64)).astype(np.float32)
+        return 0
+
+    # -------------------------------------------------------------- NVML
+    def _nvml_absent(self, *a):
+        self.err = b"NVML not available in the CPU test double"
+        return N.CQ_ERR_NVML
+
+    cq_nvml_init = cq_nvml_energy_mj = cq_nvml_power_mw = cq_nvml_sm_clock_mhz = _nvml_absent
+    cq_nvml_throttle_reasons = cq_nvml_supported_sm_clocks = _nvml_absent
+    cq_nvml_lock_sm_clock = cq_nvml_reset_sm_clock = _nvml_absent
+
+
+class LocalTransport:
+    """Single process: NCCL ops must never be issued."""
+
+    def exchange(self, ops, lib):
+        if ops:
+            raise AssertionError("NCCL op issued in a single-process run")
+
+
+class GlooTransport:
+    """NCCL group semantics over torch.distributed (gloo): all sends and
+    receives of a group are posted together, so matching across ranks must
+    be consistent or the test deadlocks / mismatches sizes."""
+
+    def exchange(self, ops, lib):
+        import torch
+        import torch.distributed as dist
+        reqs = []
+        recvs = []
+        for op, addr, n, peer in ops:
+            if op == "send":
+                t = torch.from_numpy(lib._mem(addr, n).copy())
+                reqs.append(dist.isend(t, peer))
+            else:
+                t = torch.empty(n, dtype=torch.uint8)
+                reqs.append(dist.irecv(t, peer))
+                recvs.append((addr, n, t))
+        for r in reqs:
+            r.wait()
+        for addr, n, t in recvs:
+            lib._mem(addr, n)[:] = t.numpy()
+        lib.launches.append(("group", len(ops)))

@@ -1,0 +1,150 @@
+"""Executor host logic on CPU through the numpy libcq double (tests/fakecq.py):
+single process with several nodes per device / several devices, and a real
+2-rank torch.distributed gloo run in which NCCL groups travel over gloo.
+Results must equal the reference's golden outputs bit for bit."""
+
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2505_06022_b200 as cq
+from paper_2505_06022_b200 import _native as N
+from paper_2505_06022_b200 import executor as E
+from paper_2505_06022_b200 import workloads as W
+from fakecq import FakeLib, GlooTransport, LocalTransport
+from oracle import dsl
+from progjson import graph_of, load_arrays, program_from_json
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+with open(os.path.join(GOLD, "programs.json")) as fh:
+    PROGRAMS = json.load(fh)
+EXPECTED = load_arrays(os.path.join(GOLD, "expected.npz"))
+OK_IDX = [i for i, e in enumerate(PROGRAMS) if e["error"] is None]
+
+
+@pytest.fixture
+def fake(monkeypatch):
+    def install(ndev=1, transport=None):
+        lib = FakeLib(ndev, transport or LocalTransport())
+        monkeypatch.setattr(N, "_lib", lib)
+        E._pinned.clear()
+        return lib
+    return install
+
+
+@pytest.mark.parametrize("idx", OK_IDX)
+def test_golden_programs_single_process(fake, idx):
+    entry = PROGRAMS[idx]
+    for ndev, nodes in ((1, entry["nodes"]), (2, 5)):
+        fake(ndev)
+        buffers, tasks = program_from_json(entry["program"])
+        plan = cq.generate_commands(graph_of(buffers, tasks), nodes)
+        res = E.run(plan, placement=E.Placement(1, 0, tuple(range(ndev))))
+        for name in buffers:
+            assert dsl.same_bits(res.buffers[name], EXPECTED[f"p{idx}__{name}"]), (entry["name"], name)
+
+
+def test_error_programs_raise_reference_error(fake):
+    fake(1)
+    for entry in PROGRAMS:
+        if entry["error"] is None:
+            continue
+        buffers, tasks = program_from_json(entry["program"])
+        with pytest.raises(cq.ClusterqError) as info:
+            E.run(cq.generate_commands(graph_of(buffers, tasks), entry["nodes"]))
+        assert type(info.value).__name__ == entry["error"]
+
+
+def test_wave_interior_boundary_split_and_session_rerun(fake):
+    lib = fake(1)
+    h, w = 48, 40
+    u0 = np.random.default_rng(4).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=4, kind="float32", u0=u0, up0=u0)
+    plan = cq.generate_commands(prog.graph(), 3)
+    s = E.Session(plan, E.Placement(1, 0, (0,)))
+    s.execute(upload=True)
+    s.synchronize()
+    first = s.results()
+    s.recycle()
+    # nodes 1..2 get halo rows each step: chunks split into 3 launches
+    launches = lib.launches.count("wave5")
+    assert launches > 3 * 4
+    # replay on resident data (benchmark mode): same launches, no uploads
+    s.execute(upload=False)
+    s.synchronize()
+    assert lib.launches.count("wave5") == 2 * launches
+    s.recycle()
+    # a fresh upload reproduces the first result exactly
+    s.execute(upload=True)
+    s.synchronize()
+    again = s.results()
+    s.close()
+    from oracle import native as onat
+    u, up = onat.wave_run(u0, u0, 4, 0.25)
+    assert dsl.same_bits(first["u"], u) and dsl.same_bits(first["up"], up)
+    assert dsl.same_bits(again["u"], u) and dsl.same_bits(again["up"], up)
+
+
+# ------------------------------------------------------- 2 ranks over gloo
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rank_main(rank, world, port, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = FakeLib(1, GlooTransport())
+    N._lib = lib
+    pl = E.Placement(world, rank, (0,))
+    results = {}
+    h, w = 37, 24
+    u0 = np.random.default_rng(9).uniform(0, 1, (h, w)).astype(np.float32)
+    for nodes in (2, 3):
+        prog = W.wave_program(h, w, steps=5, kind="float32", u0=u0, up0=u0)
+        res = E.run(cq.generate_commands(prog.graph(), nodes), placement=pl)
+        if rank == 0:
+            results[f"wave{nodes}_u"] = res.buffers["u"]
+            results[f"wave{nodes}_up"] = res.buffers["up"]
+        loc = E.run(cq.generate_commands(prog.graph(), nodes), placement=pl, gather="local")
+        results[f"local{nodes}_r{rank}"] = loc.buffers.get("u", np.zeros(0))
+    for idx in OK_IDX[::6]:
+        entry = PROGRAMS[idx]
+        buffers, tasks = program_from_json(entry["program"])
+        res = E.run(cq.generate_commands(graph_of(buffers, tasks), entry["nodes"]), placement=pl)
+        if rank == 0:
+            for name in buffers:
+                results[f"g{idx}__{name}"] = res.buffers[name]
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), **results)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_gloo(tmp_path):
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.start_processes(_rank_main, args=(2, port, str(tmp_path)), nprocs=2, join=True,
+                       start_method="spawn")
+    r0 = dict(np.load(tmp_path / "rank0.npz"))
+    r1 = dict(np.load(tmp_path / "rank1.npz"))
+    from oracle import native as onat
+    h, w = 37, 24
+    u0 = np.random.default_rng(9).uniform(0, 1, (h, w)).astype(np.float32)
+    u, up = onat.wave_run(u0, u0, 5, 0.25)
+    for nodes in (2, 3):
+        assert dsl.same_bits(r0[f"wave{nodes}_u"], u) and dsl.same_bits(r0[f"wave{nodes}_up"], up)
+    # gather="local": each rank holds exactly its own final rows
+    assert dsl.same_bits(r0["local2_r0"][:19], u[:19]) and dsl.same_bits(r1["local2_r1"][19:], u[19:])
+    for key, val in r0.items():
+        if key.startswith("g"):
+            idx, name = key[1:].split("__")
+            assert dsl.same_bits(val, EXPECTED[f"p{idx}__{name}"]), key

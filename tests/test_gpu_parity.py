@@ -1,0 +1,176 @@
+"""GPU parity: the B200 executor against the reference's own outputs (golden
+fixtures) and the pinned CPU oracle.  Runs on a B200 via gpurun; every call
+goes through the product path (executor -> ctypes -> libcq.so)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2505_06022_b200 as cq
+from paper_2505_06022_b200 import lowering, workloads as W
+from paper_2505_06022_b200.executor import run
+from oracle import dsl
+from oracle import native as onat
+from progjson import graph_of, load_arrays, program_from_json
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+with open(os.path.join(GOLD, "programs.json")) as fh:
+    PROGRAMS = json.load(fh)
+EXPECTED = load_arrays(os.path.join(GOLD, "expected.npz"))
+
+
+def _run_program(buffers, tasks, nodes, **kw):
+    plan = cq.generate_commands(graph_of(buffers, tasks), nodes)
+    return run(plan, **kw)
+
+
+@pytest.mark.parametrize("idx", range(len(PROGRAMS)))
+def test_reference_programs_bit_exact(idx):
+    """Every golden program (reference random workloads, bundled scenarios,
+    wave ping-pong, SAXPY) at its node count and at 1 and 5 nodes reproduces
+    the reference simulator's final buffers bit for bit."""
+    entry = PROGRAMS[idx]
+    for nodes in sorted({entry["nodes"], 1, 5}):
+        buffers, tasks = program_from_json(entry["program"])
+        if entry["error"] is not None:
+            with pytest.raises(cq.ClusterqError) as info:
+                _run_program(buffers, tasks, nodes)
+            assert type(info.value).__name__ == entry["error"]
+            return
+        res = _run_program(buffers, tasks, nodes)
+        for name in buffers:
+            assert dsl.same_bits(res.buffers[name], EXPECTED[f"p{idx}__{name}"]), \
+                (entry["name"], nodes, name)
+        n_exec = sum(1 for e in res.trace if e.kind == "execute")
+        assert n_exec == len(res.plan.executes())
+
+
+@pytest.mark.parametrize("idx", [i for i, e in enumerate(PROGRAMS) if e["error"] is None][::4])
+def test_interpreter_matches_fast_paths(idx, monkeypatch):
+    entry = PROGRAMS[idx]
+    monkeypatch.setattr(lowering, "FAST_PATHS", False)
+    buffers, tasks = program_from_json(entry["program"])
+    res = _run_program(buffers, tasks, entry["nodes"])
+    for name in buffers:
+        assert dsl.same_bits(res.buffers[name], EXPECTED[f"p{idx}__{name}"])
+
+
+@pytest.mark.parametrize("nodes", [1, 3, 4])
+def test_saxpy_f32_bit_exact(nodes):
+    n = (1 << 20) + 3
+    x, y = W.saxpy_inputs(n, "float32", seed=0)
+    prog = W.saxpy_program(n, alpha=2.0, kind="float32", x=x, y=y)
+    res = run(cq.generate_commands(prog.graph(), nodes))
+    assert dsl.same_bits(res.buffers["z"], onat.saxpy(2.0, x, y))
+
+
+def test_saxpy_baseline_config_reference_inputs():
+    """BASELINE config 1: N = 2^24, 4 chunks, x = iota, y = 1, alpha = 2:
+    z = fl32(2i + 1) exactly."""
+    n = 1 << 24
+    prog = W.saxpy_program(n, kind="float32")
+    res = run(cq.generate_commands(prog.graph(), 4))
+    want = (2.0 * np.arange(n, dtype=np.float64) + 1.0).astype(np.float32)
+    assert dsl.same_bits(res.buffers["z"], want)
+
+
+@pytest.mark.parametrize("nodes", [1, 2, 3])
+@pytest.mark.parametrize("kind", ["float32", "float64"])
+def test_wave_bit_exact_vs_oracle(nodes, kind):
+    h, w, steps = 257, 320, 7
+    dt = np.float32 if kind == "float32" else np.float64
+    u0 = np.random.default_rng(2).uniform(0, 1, (h, w)).astype(dt)
+    up0 = np.random.default_rng(5).uniform(0, 1, (h, w)).astype(dt)
+    prog = W.wave_program(h, w, steps=steps, kind=kind, c=0.25, u0=u0, up0=up0)
+    res = run(cq.generate_commands(prog.graph(), nodes))
+    u, up = onat.wave_run(u0, up0, steps, 0.25)
+    assert dsl.same_bits(res.buffers["u"], u)
+    assert dsl.same_bits(res.buffers["up"], up)
+
+
+def test_wave_unaligned_width_uses_generic_kernel():
+    h, w = 64, 37
+    u0 = np.random.default_rng(3).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=4, kind="float32", u0=u0, up0=u0)
+    res = run(cq.generate_commands(prog.graph(), 3))
+    u, up = onat.wave_run(u0, u0, 4, 0.25)
+    assert dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up)
+
+
+@pytest.mark.parametrize("nodes", [1, 3])
+def test_nbody_kick_within_tolerance(nodes):
+    n, eps2, dt = 4096, 1e-2, 1e-3
+    pos, vel = W.nbody_inputs(n)
+    prog = W.nbody_program(n, steps=1, eps2=eps2, dt=dt, pos=pos, vel=vel)
+    res = run(cq.generate_commands(prog.graph(), nodes))
+    acc = onat.nbody_accel(pos, 0, n, eps2)
+    got = res.buffers["V"][:, :3].astype(np.float64) / dt
+    err = np.linalg.norm(got - acc, axis=1) / np.linalg.norm(acc, axis=1)
+    assert err.max() <= 1e-4, err.max()
+    want_pos = pos[:, :3].astype(np.float64) + dt * res.buffers["V"][:, :3]
+    assert np.allclose(res.buffers["P"][:, :3], want_pos, rtol=0, atol=1e-6)
+    assert np.array_equal(res.buffers["P"][:, 3], pos[:, 3])
+
+
+def test_nbody_gpu_count_invariance():
+    n = 2048
+    pos, vel = W.nbody_inputs(n)
+    outs = []
+    for nodes in (1, 2, 4):
+        prog = W.nbody_program(n, steps=2, pos=pos, vel=vel)
+        outs.append(run(cq.generate_commands(prog.graph(), nodes)).buffers)
+    for o in outs[1:]:
+        assert dsl.same_bits(o["P"], outs[0]["P"]) and dsl.same_bits(o["V"], outs[0]["V"])
+
+
+@pytest.mark.parametrize("variant", ["ffma"])
+@pytest.mark.parametrize("nodes", [1, 4])
+def test_sgemm_within_tolerance(variant, nodes):
+    m, n, k = 512, 384, 256
+    a, b = W.sgemm_inputs(m, n, k)
+    prog = W.sgemm_program(m, n, k, variant=variant, a=a, b=b)
+    res = run(cq.generate_commands(prog.graph(), nodes))
+    rows = np.arange(0, m, 7)
+    c, cabs = onat.sgemm_rows(a, b, rows)
+    err = np.abs(res.buffers["C"][rows] - c) / cabs
+    assert err.max() <= 1e-6, err.max()
+
+
+def test_integer_division_by_zero_raises_eval_error():
+    ext = cq.Box.from_shape((16,))
+    bufs = {"a": cq.Buffer("a", ext, "int64", cq.BufferInit.iota()),
+            "b": cq.Buffer("b", ext, "int64", cq.BufferInit.zeros())}
+    body = {"b": cq.parse_kernel("7 / (a[i] - 5)", {"a": 1}, set(), 1)}
+    t = cq.Task("div", ext, [cq.Accessor("a", cq.AccessMode.READ), cq.Accessor("b", cq.AccessMode.WRITE)], body)
+    with pytest.raises(cq.EvalError):
+        _run_program(bufs, [t], 2)
+
+
+def test_mapper_violation_raises():
+    """A Fixed-mapped read whose clamped point leaves the declared region
+    passes the static footprint check but fails at run time
+    (ReadView.read, model.py:442-453)."""
+    ext = cq.Box.from_shape((8,))
+    bufs = {"a": cq.Buffer("a", ext, "float64", cq.BufferInit.iota()),
+            "b": cq.Buffer("b", ext, "float64", cq.BufferInit.zeros())}
+    fixed = cq.Fixed(cq.Region(1, [cq.Box((2,), (4,))]))
+    body = {"b": cq.parse_kernel("a[i-3]", {"a": 1}, set(), 1)}
+    t = cq.Task("bad", cq.Box.from_shape((2,)),
+                [cq.Accessor("a", cq.AccessMode.READ, fixed), cq.Accessor("b", cq.AccessMode.WRITE)], body)
+    with pytest.raises(cq.MapperViolationError):
+        _run_program(bufs, [t], 1)
+
+
+def test_trace_and_energy_accounting():
+    prog = W.saxpy_program(1 << 20, kind="float32")
+    plan = cq.generate_commands(prog.graph(), 4)
+    res = run(plan, energy=True)
+    kinds = [e.kind for e in res.trace]
+    assert kinds.count("execute") == 4 and kinds.count("push") == kinds.count("await_push") == 6
+    assert res.makespan > 0
+    rep = cq.account_energy(res.trace, plan.devices, res.makespan)
+    assert rep.total_kernel_energy + rep.total_idle_energy == rep.total_device_energy
