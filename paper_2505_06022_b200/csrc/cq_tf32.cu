@@ -1,14 +1,351 @@
-// 3xTF32 SGEMM on tcgen05 (placeholder until the tensor-core path lands).
+// 3xTF32 SGEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// C[m,n] = A[m,k] . B[k,n] in fp32 accuracy from TF32 products:
+//   a = a_hi + a_lo with a_hi = a with the low 13 mantissa bits cleared
+//   (exactly representable in TF32) and a_lo = a - a_hi (exact in fp32);
+//   C ~= a_hi*b_hi + a_hi*b_lo + a_lo*b_hi   (a_lo*b_lo ~ 2^-22 |ab| dropped)
+// accumulated in fp32 in TMEM.  This is the matmul of BASELINE config 3
+// (slice-mapped): the normalised error |C - C64| / sum|a||b|
+// stays ~1e-8, where plain 1xTF32 (~5e-6 at K = 16384) fails the 1e-6 bar.
+//
+// Structure (one CTA per 128 x BN output tile, 1 CTA / SM):
+//   split pass : A -> A_hi, A_lo ([m,k], K-major); B -> Bt_hi, Bt_lo ([n,k],
+//                transposed to K-major), one HBM pass each;
+//   warp 0     : TMA producer, 4 tiles (A_hi, A_lo, B_hi, B_lo) per 32-wide k
+//                block into a STAGES-deep ring, 128-byte swizzle;
+//   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer,
+//                3 MMAs (M=128, N=BN, K=8) per 8-wide k step, commits free the
+//                smem stage; the last commit signals the epilogue;
+//   warps 2-5  : epilogue, tcgen05.ld 32x32b.x32 TMEM -> registers -> C.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "cq_common.cuh"
 
 namespace cq {
+namespace tf32 {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements = 128 bytes = one swizzle atom row
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// K-major operand tile, 128-byte swizzle: rows of 128 B, 8-row groups 1024 B
+// apart (SBO), LBO unused for swizzled K-major; descriptor version 1 (sm_100).
+__device__ __forceinline__ uint64_t smem_desc(const void* tile) {
+  uint64_t addr = smem_u32(tile);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;          // start address      [0,14)
+  d |= (uint64_t)1 << 16;                  // LBO (ignored)      [16,30)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO = 1024 B       [32,46)
+  d |= (uint64_t)1 << 46;                  // version            [46,48)
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B       [61,64)
+  return d;
+}
+
+// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, K-major both.
+__host__ __device__ constexpr uint32_t instr_desc(int m, int n) {
+  return (1u << 4)                    // c_format = F32
+         | (2u << 7)                  // a_format = TF32
+         | (2u << 10)                 // b_format = TF32
+         | ((uint32_t)(n >> 3) << 17)  // N >> 3
+         | ((uint32_t)(m >> 4) << 24); // M >> 4
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int BN, int STAGES>
+struct Smem {
+  float a_hi[STAGES][BM * BK];
+  float a_lo[STAGES][BM * BK];
+  float b_hi[STAGES][BN * BK];
+  float b_lo[STAGES][BN * BK];
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tmem_full;
+  uint32_t tmem_base;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                        const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                        float* __restrict__ C, int64_t ldc, int m, int n, int k) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte alignment for the 128-byte swizzle atoms
+  Smem<BN, STAGES>& S = *reinterpret_cast<Smem<BN, STAGES>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile_n = blockIdx.x, tile_m = blockIdx.y;
+  const int num_kb = (k + BK - 1) / BK;
+  constexpr uint32_t kStageBytes = (2 * BM * BK + 2 * BN * BK) * sizeof(float);
+  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_ahi);
+    prefetch_map(&map_alo);
+    prefetch_map(&map_bhi);
+    prefetch_map(&map_blo);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], 1);
+    }
+    mbar_init(&S.tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&S.empty[s], phase ^ 1);
+        mbar_expect_tx(&S.full[s], kStageBytes);
+        const int kc = kb * BK;
+        tma_load_2d(S.a_hi[s], &map_ahi, &S.full[s], kc, tile_m * BM);
+        tma_load_2d(S.a_lo[s], &map_alo, &S.full[s], kc, tile_m * BM);
+        tma_load_2d(S.b_hi[s], &map_bhi, &S.full[s], kc, tile_n * BN);
+        tma_load_2d(S.b_lo[s], &map_blo, &S.full[s], kc, tile_n * BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = instr_desc(BM, BN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&S.full[s], phase);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t dah = smem_desc(S.a_hi[s]), dal = smem_desc(S.a_lo[s]);
+        const uint64_t dbh = smem_desc(S.b_hi[s]), dbl = smem_desc(S.b_lo[s]);
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          // advance 8 fp32 = 32 bytes inside the swizzle atom: +2 in addr>>4
+          const uint64_t o = (uint64_t)(kk * 2);
+          mma_tf32(tmem, dah + o, dbh + o, idesc, (kb | kk) != 0);
+          mma_tf32(tmem, dah + o, dbl + o, idesc, 1);
+          mma_tf32(tmem, dal + o, dbh + o, idesc, 1);
+        }
+        mma_commit(&S.empty[s]);
+      }
+      mma_commit(&S.tmem_full);
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +32 (rows of the tile)
+    mbar_wait(&S.tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int lane_group = warp & 3;
+    const int row = tile_m * BM + lane_group * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(lane_group * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+            "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+            "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+            "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      const int col = tile_n * BN + c0;
+      if (row < m) {
+        float* dst = C + (int64_t)row * ldc + col;
+        if (col + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            reinterpret_cast<float4*>(dst)[q] =
+                make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                            __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (col + q < n) dst[q] = __uint_as_float(r[q]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------- split pass
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// A [m,k] (lda) -> hi, lo [m,k] dense (k contiguous)
+__global__ void split_rows_kernel(const float* __restrict__ a, int64_t lda, float* __restrict__ hi,
+                                  float* __restrict__ lo, int64_t m, int64_t k) {
+  int64_t total = m * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = t / k, c = t % k;
+    float x = a[r * lda + c];
+    float h = tf32_hi(x);
+    hi[t] = h;
+    lo[t] = x - h;
+  }
+}
+
+// B [k,n] (ldb) -> hi, lo transposed [n,k] dense, via 32x32 shared tiles
+__global__ void split_transpose_kernel(const float* __restrict__ b, int64_t ldb, float* __restrict__ hi,
+                                       float* __restrict__ lo, int64_t k, int64_t n) {
+  __shared__ float tile[32][33];
+  int64_t k0 = (int64_t)blockIdx.y * 32, n0 = (int64_t)blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t kk = k0 + i, nn = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (kk < k && nn < n) ? b[kk * ldb + nn] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t nn = n0 + i, kk = k0 + threadIdx.x;
+    if (nn < n && kk < k) {
+      float x = tile[threadIdx.x][i];
+      float h = tf32_hi(x);
+      hi[nn * k + kk] = h;
+      lo[nn * k + kk] = x - h;
+    }
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major fp32 [rows, cols] (cols contiguous), box = [BK cols, box_rows].
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows) {
+  auto encode = get_encode();
+  if (!encode) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return CQ_ERR_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return CQ_ERR_CUDA;
+  }
+  return CQ_OK;
+}
+
+template <int BN, int STAGES>
+static int launch(cudaStream_t st, const float* ahi, const float* alo, const float* bhi, const float* blo, float* c,
+                  int64_t ldc, int64_t m, int64_t n, int64_t k) {
+  CUtensorMap ma, mal, mb, mbl;
+  CQ_TRY(make_map(&ma, ahi, m, k, BM));
+  CQ_TRY(make_map(&mal, alo, m, k, BM));
+  CQ_TRY(make_map(&mb, bhi, n, k, BN));
+  CQ_TRY(make_map(&mbl, blo, n, k, BN));
+  size_t smem = sizeof(Smem<BN, STAGES>) + 1024;
+  auto kern = sgemm_3xtf32_kernel<BN, STAGES>;
+  CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM));
+  kern<<<grid, kThreads, smem, st>>>(ma, mal, mb, mbl, c, ldc, (int)m, (int)n, (int)k);
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+}  // namespace tf32
 
 int sgemm_3xtf32(cudaStream_t st, int sm_count, const float* a, int64_t lda, const float* b, int64_t ldb,
                  float* c, int64_t ldc, int64_t m, int64_t n, int64_t k) {
-  (void)st; (void)sm_count; (void)a; (void)lda; (void)b; (void)ldb; (void)c; (void)ldc;
-  (void)m; (void)n; (void)k;
-  set_error("cq_sgemm: 3xTF32 variant not built yet");
-  return CQ_ERR_UNSUPPORTED;
+  (void)sm_count;
+  CQ_REQUIRE(k % 4 == 0, "3xTF32 sgemm needs k %% 4 == 0 (16-byte TMA row pitch)");
+  CQ_REQUIRE(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), "3xTF32 sgemm: dims exceed int32");
+  // scratch for the split operands: 2*(m+n)*k floats, stream-ordered
+  float* scratch = nullptr;
+  size_t bytes = (size_t)2 * (size_t)(m + n) * (size_t)k * sizeof(float);
+  CQ_CHECK_CUDA(cudaMallocAsync(&scratch, bytes, st));
+  float* ahi = scratch;
+  float* alo = ahi + m * k;
+  float* bhi = alo + m * k;
+  float* blo = bhi + n * k;
+  tf32::split_rows_kernel<<<sm_count * 8, 256, 0, st>>>(a, lda, ahi, alo, m, k);
+  CQ_CHECK_LAUNCH();
+  dim3 tg((unsigned)((n + 31) / 32), (unsigned)((k + 31) / 32));
+  tf32::split_transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(b, ldb, bhi, blo, k, n);
+  CQ_CHECK_LAUNCH();
+  int status = (n >= 256) ? tf32::launch<256, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
+                          : tf32::launch<128, 3>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+  cudaFreeAsync(scratch, st);
+  return status;
 }
 
 }  // namespace cq
