@@ -219,6 +219,10 @@ def bench_wave(args, dist, placement, peaks):
     kern_bytes = sum(12 * cells for _k, cells, *_ in wave_launches)
     dom_launch = max(wave_launches, key=lambda x: x[1])
     sess.recycle()
+    energy = energy_loop(sess, 1.5) if args.energy else None
+    if energy and "j_per_iter" in energy:
+        energy["j_per_time_step"] = energy["j_per_iter"] / steps
+        energy["gb_per_joule"] = 12 * H * Wd * steps / 1e9 / energy["j_per_iter"] / world
     sess.close()
     dev_ms = dist.max(dev_ms)
     cells = H * Wd * steps * args.steps
@@ -265,6 +269,7 @@ def bench_wave(args, dist, placement, peaks):
                      "peak_source": peaks[1] + " hbm_gbs (torch copy)"},
         "clocks": clk,
         "gpu_launches": gpu_launches,
+        "energy": energy,
         "H": H, "W": Wd,
     }
 
@@ -506,6 +511,10 @@ def main():
                        "plan_s": wave["plan_s"], "init": "Gaussian pulse (SURVEY.md §8d)"},
             "e2e": wave["e2e"], "roofline": wave["roofline"], "cpu_baseline": cpu,
             "clocks": wave["clocks"], "gpu_launches": wave["gpu_launches"],
+            "energy": {"wave5": wave["energy"],
+                       "clock_sweep": "not run: SM clock locking is disabled on this shared pool "
+                                      "(cq_nvml_lock_sm_clock requires CQ_ALLOW_CLOCK_LOCK=1); "
+                                      "J/iteration reported at the running clock"},
             "kernels": kernels,
         }
         print(json.dumps(line))

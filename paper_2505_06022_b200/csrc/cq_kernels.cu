@@ -348,14 +348,22 @@ __global__ void __launch_bounds__(128) expr_kernel(const __grid_constant__ cq_ex
 // memory and every lane reads them back by broadcast (LDS.128); partial
 // accelerations are summed over the warps in fixed order.
 constexpr int NB_WARPS = 8;
-constexpr int NB_IPT = 2;
+constexpr int NB_IPT = 4;
 constexpr int NB_IBLOCK = 32 * NB_IPT;
+
+// r2 >= eps2 > 0, so the flush-to-zero approximate reciprocal square root
+// needs no denormal guard: one MUFU.RSQ per interaction.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ void nb_interact(const float4& pi, const float4& pj, float eps2, float& ax,
                                             float& ay, float& az) {
   float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
   float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
-  float inv = rsqrtf(r2);
+  float inv = rsqrt_ftz(r2);
   float s = pj.w * (inv * inv * inv);
   ax = fmaf(dx, s, ax);
   ay = fmaf(dy, s, ay);

@@ -15,9 +15,13 @@
 //                block into a STAGES-deep ring, 128-byte swizzle;
 //   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer,
 //                3 MMAs (M=128, N=BN, K=8) per 8-wide k step, commits free the
-//                smem stage; the last commit signals the epilogue;
-//   warps 2-5  : epilogue, tcgen05.ld 32x32b.x32 TMEM -> registers -> C.
+//                smem stage; every `group_kb` k blocks the accumulator buffer
+//                (one of two in TMEM) is handed to the epilogue;
+//   warps 2..  : 4*BN/64 epilogue warps (32 rows x 64 columns each) drain
+//                each finished group with tcgen05.ld into fp32 registers
+//                (round-to-nearest adds), then store C once.
 #include <cuda.h>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "cq_common.cuh"
@@ -27,7 +31,6 @@ namespace tf32 {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements = 128 bytes = one swizzle atom row
-constexpr int kThreads = 192;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -104,6 +107,22 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// The tensor core's fp32 accumulation truncates; a single TMEM accumulator
+// over K = 16384 (6144 MMAs) builds a bias of ~6e-6 (normalised).  So K is
+// processed in groups of `group_kb` 32-wide k blocks: each group accumulates
+// in one of two TMEM buffers while the epilogue warps drain the other into
+// round-to-nearest fp32 registers (FADD).  Error ~1e-7 at K = 16384.
+template <int BN>
+struct Epi {
+  static constexpr int kWarps = 4 * (BN / 64);   // 32 rows x 64 columns each
+  static constexpr int kThreads = 64 + 32 * kWarps;
+  static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
+};
+
 template <int BN, int STAGES>
 struct Smem {
   float a_hi[STAGES][BM * BK];
@@ -112,15 +131,25 @@ struct Smem {
   float b_lo[STAGES][BN * BK];
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
-  uint64_t tmem_full;
+  uint64_t tfull[2];
+  uint64_t tempty[2];
   uint32_t tmem_base;
 };
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
     sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                         const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
-                        float* __restrict__ C, int64_t ldc, int m, int n, int k) {
+                        float* __restrict__ C, int64_t ldc, int m, int n, int k, int group_kb) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128-byte swizzle atoms
   Smem<BN, STAGES>& S = *reinterpret_cast<Smem<BN, STAGES>*>(
@@ -128,8 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile_n = blockIdx.x, tile_m = blockIdx.y;
   const int num_kb = (k + BK - 1) / BK;
+  const int num_groups = (num_kb + group_kb - 1) / group_kb;
   constexpr uint32_t kStageBytes = (2 * BM * BK + 2 * BN * BK) * sizeof(float);
-  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_ahi);
@@ -140,12 +169,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&S.full[s], 1);
       mbar_init(&S.empty[s], 1);
     }
-    mbar_init(&S.tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.tfull[b], 1);
+      mbar_init(&S.tempty[b], Epi<BN>::kWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
-                 "r"(kTmemCols));
+                 "r"(Epi<BN>::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -170,60 +202,70 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = instr_desc(BM, BN);
-      for (int kb = 0; kb < num_kb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t phase = (kb / STAGES) & 1;
-        mbar_wait(&S.full[s], phase);
+      int kb = 0;
+      for (int g = 0; g < num_groups; ++g) {
+        const int buf = g & 1;
+        mbar_wait(&S.tempty[buf], ((g >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t dah = smem_desc(S.a_hi[s]), dal = smem_desc(S.a_lo[s]);
-        const uint64_t dbh = smem_desc(S.b_hi[s]), dbl = smem_desc(S.b_lo[s]);
+        const uint32_t acc_addr = tmem + (uint32_t)(buf * BN);
+        const int kb_end = min(kb + group_kb, num_kb);
+        for (int first = kb; kb < kb_end; ++kb) {
+          const int s = kb % STAGES;
+          const uint32_t phase = (kb / STAGES) & 1;
+          mbar_wait(&S.full[s], phase);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t dah = smem_desc(S.a_hi[s]), dal = smem_desc(S.a_lo[s]);
+          const uint64_t dbh = smem_desc(S.b_hi[s]), dbl = smem_desc(S.b_lo[s]);
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          // advance 8 fp32 = 32 bytes inside the swizzle atom: +2 in addr>>4
-          const uint64_t o = (uint64_t)(kk * 2);
-          mma_tf32(tmem, dah + o, dbh + o, idesc, (kb | kk) != 0);
-          mma_tf32(tmem, dah + o, dbl + o, idesc, 1);
-          mma_tf32(tmem, dal + o, dbh + o, idesc, 1);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            // advance 8 fp32 = 32 bytes inside the swizzle atom: +2 in addr>>4
+            const uint64_t o = (uint64_t)(kk * 2);
+            mma_tf32(acc_addr, dah + o, dbh + o, idesc, (kb != first || kk != 0) ? 1u : 0u);
+            mma_tf32(acc_addr, dah + o, dbl + o, idesc, 1);
+            mma_tf32(acc_addr, dal + o, dbh + o, idesc, 1);
+          }
+          mma_commit(&S.empty[s]);
         }
-        mma_commit(&S.empty[s]);
+        mma_commit(&S.tfull[buf]);
       }
-      mma_commit(&S.tmem_full);
     }
   } else {
-    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +32 (rows of the tile)
-    mbar_wait(&S.tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue warp e: TMEM lanes 32*(warp%4).. (tile rows), columns 64*seg..
+    const int e = warp - 2;
     const int lane_group = warp & 3;
+    const int seg = e >> 2;
+    float acc[64];
+#pragma unroll
+    for (int q = 0; q < 64; ++q) acc[q] = 0.f;
+    for (int g = 0; g < num_groups; ++g) {
+      const int buf = g & 1;
+      mbar_wait(&S.tfull[buf], (g >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = tmem + ((uint32_t)(lane_group * 32) << 16) + (uint32_t)(buf * BN + seg * 64);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t r[16];
+        tmem_ld16(base + (uint32_t)(h * 16), r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[h * 16 + q] += __uint_as_float(r[q]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.tempty[buf]);
+    }
     const int row = tile_m * BM + lane_group * 32 + lane;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + ((uint32_t)(lane_group * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-          "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
-            "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
-            "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
-            "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      const int col = tile_n * BN + c0;
-      if (row < m) {
-        float* dst = C + (int64_t)row * ldc + col;
-        if (col + 32 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+    const int col = tile_n * BN + seg * 64;
+    if (row < m) {
+      float* dst = C + (int64_t)row * ldc + col;
+      if (col + 64 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            reinterpret_cast<float4*>(dst)[q] =
-                make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                            __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-        } else {
+        for (int q = 0; q < 16; ++q)
+          reinterpret_cast<float4*>(dst)[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      } else {
 #pragma unroll
-          for (int q = 0; q < 32; ++q)
-            if (col + q < n) dst[q] = __uint_as_float(r[q]);
-        }
+        for (int q = 0; q < 64; ++q)
+          if (col + q < n) dst[q] = acc[q];
       }
     }
   }
@@ -231,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Epi<BN>::kTmemCols));
   }
 }
 
@@ -317,7 +359,9 @@ static int launch(cudaStream_t st, const float* ahi, const float* alo, const flo
   auto kern = sgemm_3xtf32_kernel<BN, STAGES>;
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM));
-  kern<<<grid, kThreads, smem, st>>>(ma, mal, mb, mbl, c, ldc, (int)m, (int)n, (int)k);
+  int group_kb = 4;  // K = 128 per TMEM accumulation group
+  if (const char* g = getenv("CQ_TF32_GROUP_KB")) group_kb = atoi(g) > 0 ? atoi(g) : group_kb;
+  kern<<<grid, Epi<BN>::kThreads, smem, st>>>(ma, mal, mb, mbl, c, ldc, (int)m, (int)n, (int)k, group_kb);
   CQ_CHECK_LAUNCH();
   return CQ_OK;
 }
@@ -342,8 +386,10 @@ int sgemm_3xtf32(cudaStream_t st, int sm_count, const float* a, int64_t lda, con
   dim3 tg((unsigned)((n + 31) / 32), (unsigned)((k + 31) / 32));
   tf32::split_transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(b, ldb, bhi, blo, k, n);
   CQ_CHECK_LAUNCH();
-  int status = (n >= 256) ? tf32::launch<256, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
-                          : tf32::launch<128, 3>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+  const char* bn = getenv("CQ_TF32_BN");
+  bool wide = n >= 256 && !(bn && atoi(bn) == 128);
+  int status = wide ? tf32::launch<256, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
+                    : tf32::launch<128, 3>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
   cudaFreeAsync(scratch, st);
   return status;
 }
