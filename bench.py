@@ -287,11 +287,13 @@ def _timed_session(plan, placement, dist, reps, warm=2):
         sess.synchronize()
         sess.recycle()
     dist.barrier()
-    m0 = sess.mark()
-    for _ in range(reps):
-        sess.execute(upload=False)
-    m1 = sess.mark()
-    sess.synchronize()
+    with ClockSampler(placement.devices[0]) as clocks:
+        m0 = sess.mark()
+        for _ in range(reps):
+            sess.execute(upload=False)
+        m1 = sess.mark()
+        sess.synchronize()
+    sess.clocks = clocks.summary()
     ms = max(sess.elapsed_ms(m0[d], m1[d]) for d in sess.devices)
     log = list(sess.launch_log)
     per_kind = {}
@@ -361,21 +363,26 @@ def bench_kernels(args, dist, placement, peaks):
     prog = W.nbody_program(nb, steps=3)
     plan = cq.generate_commands(prog.graph(), world)
     sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=3, warm=1)
-    k = kinds.get("native", [0, 1.0, 1])
+    clocks = sess.clocks
+    kick = kinds.get("nbody.kick", [0, 1.0, 1])
     inter = nb * nb * 3 * 3
     gflops = 20 * inter / (ms / 1e3) / 1e9
+    kick_gflops = dist.min(20 * (kick[0] // 4) * nb / (kick[1] / 1e3) / 1e9)
     energy = energy_loop(sess, 1.0) if args.energy else None
-    clk = (energy or {}).get("sm_clock_mhz") or sm_mhz
+    clk = clocks.get("sm_mhz") or (energy or {}).get("sm_clock_mhz")
     out["nbody_262144"] = {"value": gflops, "unit": "GFLOP/s", "scaling": "strong",
                            "ms_per_step": ms / 9, "flop_per_interaction": 20,
-                           "fp32_peak_tflops_at_max_clock": fp32_peak(1965),
-                           "frac_of_fp32_peak_at_max_clock": gflops / 1e3 / fp32_peak(1965),
-                           "frac_of_fp32_peak_at_observed_clock":
-                               (gflops / 1e3 / fp32_peak(clk)) if clk else None,
-                           "observed_sm_mhz": clk, "energy": energy}
+                           "roofline": {"bound": "fp32", "achieved": kick_gflops,
+                                        "peak": fp32_peak(1965) * 1e3, "unit": "GFLOP/s",
+                                        "frac": kick_gflops / 1e3 / fp32_peak(1965),
+                                        "frac_at_observed_clock":
+                                            (kick_gflops / 1e3 / fp32_peak(clk)) if clk else None,
+                                        "peak_definition": "148 SM x 128 FP32 lanes x 2 flop x 1965 MHz"},
+                           "clocks": clocks, "energy": energy}
     sess.close()
 
-    # sgemm 16384^3 (slice mappers), FFMA (tcgen05 3xTF32 reported when built)
+    # sgemm 16384^3 (slice mappers): 3xTF32 on tcgen05 and the FFMA baseline
+    tf32_ceiling = peaks[0].get("bf16_tflops", 1666.6) / 2 / 3
     for variant in args.sgemm_variants:
         m = args.sgemm
         a = np.empty((m, m), np.float32)
@@ -391,8 +398,14 @@ def bench_kernels(args, dist, placement, peaks):
             out[f"sgemm_{variant}"] = {"error": str(exc)}
             continue
         tflops = 2 * m ** 3 * 3 / (ms / 1e3) / 1e12
-        out[f"sgemm_{variant}_{m}"] = {"value": tflops * 1e3, "unit": "GFLOP/s", "scaling": "strong",
-                                       "frac_of_fp32_peak_at_max_clock": tflops / fp32_peak(1965)}
+        entry = {"value": tflops * 1e3, "unit": "GFLOP/s (useful 2MNK)", "scaling": "strong",
+                 "frac_of_fp32_simt_peak_at_max_clock": tflops / fp32_peak(1965),
+                 "clocks": sess.clocks}
+        if variant == "3xtf32":
+            entry["roofline"] = {"bound": "tensor", "achieved": tflops, "unit": "TFLOP/s",
+                                 "peak": tf32_ceiling, "frac": tflops / tf32_ceiling,
+                                 "peak_definition": "measured bf16 dense / 2 (TF32) / 3 (products)"}
+        out[f"sgemm_{variant}_{m}"] = entry
         sess.close()
     return out
 

@@ -91,6 +91,29 @@ void oracle_nbody_accel(const float* pos, int64_t n, int64_t i0, int64_t i1, dou
   }
 }
 
+/* Same as oracle_nbody_accel for an explicit list of i-bodies. */
+void oracle_nbody_accel_idx(const float* pos, int64_t n, const int64_t* idx, int64_t count, double eps2,
+                            double* acc) {
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int64_t q = 0; q < count; ++q) {
+    int64_t i = idx[q];
+    double px = pos[4 * i], py = pos[4 * i + 1], pz = pos[4 * i + 2];
+    double ax = 0, ay = 0, az = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      double dx = (double)pos[4 * j] - px, dy = (double)pos[4 * j + 1] - py, dz = (double)pos[4 * j + 2] - pz;
+      double r2 = dx * dx + dy * dy + dz * dz + eps2;
+      double inv = 1.0 / sqrt(r2);
+      double s = (double)pos[4 * j + 3] * inv * inv * inv;
+      ax += dx * s;
+      ay += dy * s;
+      az += dz * s;
+    }
+    acc[3 * q] = ax;
+    acc[3 * q + 1] = ay;
+    acc[3 * q + 2] = az;
+  }
+}
+
 /* C rows: c[r, :] = sum_k a[r, k] * b[k, :] in float64, k ascending; also
  * returns sum_k |a[r,k]| |b[k,:]| for the normalised error metric. */
 void oracle_sgemm_rows(const float* a, const float* b, int64_t n, int64_t k, const int64_t* rows,

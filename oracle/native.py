@@ -42,6 +42,7 @@ def lib():
         L.oracle_wave5_f32.argtypes = [P, P, P, i64, i64, i64, i64, ctypes.c_float, ctypes.c_float,
                                        ctypes.c_float]
         L.oracle_nbody_accel.argtypes = [P, i64, i64, i64, ctypes.c_double, P]
+        L.oracle_nbody_accel_idx.argtypes = [P, i64, P, i64, ctypes.c_double, P]
         L.oracle_sgemm_rows.argtypes = [P, P, i64, i64, P, i64, P, P]
         _lib = L
     return _lib
@@ -91,6 +92,14 @@ def nbody_accel(pos, i0, i1, eps2):
     pos = np.ascontiguousarray(pos, dtype=np.float32)
     acc = np.empty((i1 - i0, 3), np.float64)
     lib().oracle_nbody_accel(_p(pos), pos.shape[0], i0, i1, ctypes.c_double(eps2), _p(acc))
+    return acc
+
+
+def nbody_accel_idx(pos, idx, eps2):
+    pos = np.ascontiguousarray(pos, dtype=np.float32)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    acc = np.empty((idx.size, 3), np.float64)
+    lib().oracle_nbody_accel_idx(_p(pos), pos.shape[0], _p(idx), idx.size, ctypes.c_double(eps2), _p(acc))
     return acc
 
 

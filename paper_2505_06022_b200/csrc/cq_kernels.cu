@@ -359,53 +359,104 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
   return y;
 }
 
-__device__ __forceinline__ void nb_interact(const float4& pi, const float4& pj, float eps2, float& ax,
-                                            float& ay, float& az) {
-  float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-  float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
-  float inv = rsqrt_ftz(r2);
-  float s = pj.w * (inv * inv * inv);
-  ax = fmaf(dx, s, ax);
-  ay = fmaf(dy, s, ay);
-  az = fmaf(dz, s, az);
+// Blackwell packed FP32 (FADD2/FMUL2/FFMA2): each instruction applies the
+// same IEEE round-to-nearest operation to two independent lanes, so a lane
+// pair of i-bodies costs half the issue slots with per-body results identical
+// to the scalar formulation.
+typedef unsigned long long f32x2;
+
+__device__ __forceinline__ f32x2 pack2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack2(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// one j-body (duplicated into both lanes) against a pair of i-bodies:
+//   d = p_j - p_i; r2 = d.d + eps2; s = m_j * (inv*inv*inv), inv = rsqrt(r2)
+//   a += d * s          (20 flop / interaction by the GPU Gems convention)
+__device__ __forceinline__ void nb_interact2(f32x2 pix, f32x2 piy, f32x2 piz, f32x2 jx, f32x2 jy, f32x2 jz,
+                                             f32x2 jm, f32x2 eps2, f32x2& ax, f32x2& ay, f32x2& az) {
+  f32x2 dx = sub2(jx, pix), dy = sub2(jy, piy), dz = sub2(jz, piz);
+  f32x2 r2 = fma2(dx, dx, fma2(dy, dy, fma2(dz, dz, eps2)));
+  float rl, rh;
+  unpack2(r2, rl, rh);
+  f32x2 inv = pack2(rsqrt_ftz(rl), rsqrt_ftz(rh));
+  f32x2 s = mul2(jm, mul2(mul2(inv, inv), inv));
+  ax = fma2(dx, s, ax);
+  ay = fma2(dy, s, ay);
+  az = fma2(dz, s, az);
 }
 
 __global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4* __restrict__ pos,
                                                                    int64_t n, const float4* vel_in,
                                                                    float4* vel, int64_t i_lo,
                                                                    int64_t i_hi, float eps2, float dt) {
-  __shared__ float4 tile[NB_WARPS][32];
+  constexpr int NP = NB_IPT / 2;  // i-body pairs per lane
+  // j tile, each body duplicated for the packed lanes: (x,x,y,y), (z,z,m,m)
+  __shared__ __align__(16) float4 tile[NB_WARPS][32][2];
   __shared__ float part[NB_WARPS][3][NB_IBLOCK];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ibase = i_lo + (int64_t)blockIdx.x * NB_IBLOCK;
-  float4 pi[NB_IPT];
-  float ax[NB_IPT], ay[NB_IPT], az[NB_IPT];
+  f32x2 px[NP], py[NP], pz[NP], ax[NP], ay[NP], az[NP];
 #pragma unroll
-  for (int q = 0; q < NB_IPT; ++q) {
-    int64_t i = ibase + lane + 32 * q;
-    pi[q] = pos[i < i_hi ? i : i_hi - 1];
-    ax[q] = ay[q] = az[q] = 0.f;
+  for (int p = 0; p < NP; ++p) {
+    int64_t i0 = ibase + lane + 32 * (2 * p), i1 = i0 + 32;
+    float4 a = pos[i0 < i_hi ? i0 : i_hi - 1];
+    float4 b = pos[i1 < i_hi ? i1 : i_hi - 1];
+    px[p] = pack2(a.x, b.x);
+    py[p] = pack2(a.y, b.y);
+    pz[p] = pack2(a.z, b.z);
+    ax[p] = ay[p] = az[p] = 0ull;
   }
+  const f32x2 e2 = pack2(eps2, eps2);
   const int64_t jb = (n * warp) / NB_WARPS, je = (n * (warp + 1)) / NB_WARPS;
   float4 next = (jb + lane < je) ? pos[jb + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t j0 = jb; j0 < je; j0 += 32) {
-    tile[warp][lane] = next;
+    tile[warp][lane][0] = make_float4(next.x, next.x, next.y, next.y);
+    tile[warp][lane][1] = make_float4(next.z, next.z, next.w, next.w);
     __syncwarp();
     int64_t jn = j0 + 32 + lane;
     next = (jn < je) ? pos[jn] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 16
+#pragma unroll 8
     for (int k = 0; k < 32; ++k) {
-      float4 pj = tile[warp][k];
+      const ulonglong2 xy = *reinterpret_cast<const ulonglong2*>(&tile[warp][k][0]);
+      const ulonglong2 zm = *reinterpret_cast<const ulonglong2*>(&tile[warp][k][1]);
 #pragma unroll
-      for (int q = 0; q < NB_IPT; ++q) nb_interact(pi[q], pj, eps2, ax[q], ay[q], az[q]);
+      for (int p = 0; p < NP; ++p)
+        nb_interact2(px[p], py[p], pz[p], xy.x, xy.y, zm.x, zm.y, e2, ax[p], ay[p], az[p]);
     }
     __syncwarp();
   }
 #pragma unroll
-  for (int q = 0; q < NB_IPT; ++q) {
-    part[warp][0][lane + 32 * q] = ax[q];
-    part[warp][1][lane + 32 * q] = ay[q];
-    part[warp][2][lane + 32 * q] = az[q];
+  for (int p = 0; p < NP; ++p) {
+    float lo, hi;
+    unpack2(ax[p], lo, hi);
+    part[warp][0][lane + 64 * p] = lo;
+    part[warp][0][lane + 64 * p + 32] = hi;
+    unpack2(ay[p], lo, hi);
+    part[warp][1][lane + 64 * p] = lo;
+    part[warp][1][lane + 64 * p + 32] = hi;
+    unpack2(az[p], lo, hi);
+    part[warp][2][lane + 64 * p] = lo;
+    part[warp][2][lane + 64 * p + 32] = hi;
   }
   __syncthreads();
   if (threadIdx.x < NB_IBLOCK) {

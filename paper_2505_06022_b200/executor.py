@@ -699,7 +699,8 @@ class Session:
                                binding, task, cmd, box, dev, stream, rviews, wviews, reads))
             marks.append(t)
             if self.want_trace:
-                self.launch_log.append((binding.kind, box.volume(), dev, stream, t[0], t[1]))
+                kind = binding.args["name"] if binding.kind == "native" else binding.kind
+                self.launch_log.append((kind, box.volume(), dev, stream, t[0], t[1]))
         if self.want_trace:
             self.trace_marks.append((cmd, node, dev, marks, None))
 

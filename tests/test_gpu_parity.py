@@ -127,7 +127,7 @@ def test_nbody_gpu_count_invariance():
         assert dsl.same_bits(o["P"], outs[0]["P"]) and dsl.same_bits(o["V"], outs[0]["V"])
 
 
-@pytest.mark.parametrize("variant", ["ffma"])
+@pytest.mark.parametrize("variant", ["ffma", "3xtf32"])
 @pytest.mark.parametrize("nodes", [1, 4])
 def test_sgemm_within_tolerance(variant, nodes):
     m, n, k = 512, 384, 256
@@ -174,3 +174,31 @@ def test_trace_and_energy_accounting():
     assert res.makespan > 0
     rep = cq.account_energy(res.trace, plan.devices, res.makespan)
     assert rep.total_kernel_energy + rep.total_idle_energy == rep.total_device_energy
+
+
+def test_nbody_baseline_size_sampled():
+    """BASELINE config 2 size: 262,144 bodies; 1,024 sampled i-bodies x all
+    j against the float64 oracle (SURVEY.md §8d tolerance 1e-4)."""
+    n, eps2, dt = 262144, 1e-2, 1e-3
+    pos, vel = W.nbody_inputs(n)
+    prog = W.nbody_program(n, steps=1, eps2=eps2, dt=dt, pos=pos, vel=vel)
+    res = run(cq.generate_commands(prog.graph(), 1))
+    idx = np.random.default_rng(0).choice(n, 1024, replace=False)
+    got = res.buffers["V"][idx, :3].astype(np.float64) / dt
+    want = onat.nbody_accel_idx(pos, idx, eps2)
+    err = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+    assert err.max() <= 1e-4, err.max()
+
+
+@pytest.mark.parametrize("variant", ["3xtf32", "ffma"])
+def test_sgemm_baseline_size_sampled(variant):
+    """BASELINE config 3 size: 16384^3 fp32; 256 sampled rows of C against a
+    float64 oracle, |C - C64| / sum|a||b| <= 1e-6."""
+    m = 16384
+    a, b = W.sgemm_inputs(m, m, m)
+    prog = W.sgemm_program(m, m, m, variant=variant, a=a, b=b)
+    res = run(cq.generate_commands(prog.graph(), 1), trace=False)
+    rows = np.random.default_rng(1).choice(m, 256, replace=False)
+    c, cabs = onat.sgemm_rows(a, b, rows)
+    err = np.abs(res.buffers["C"][rows] - c) / cabs
+    assert err.max() <= 1e-6, err.max()
