@@ -1,0 +1,57 @@
+"""report.json schema (reference cli.py:85-115) and the measured-table
+frequency policy (reference selection rule, energy.py:93-106)."""
+
+import json
+from fractions import Fraction
+
+import pytest
+
+import paper_2505_06022_b200 as cq
+from paper_2505_06022_b200 import _native as N
+from paper_2505_06022_b200 import executor as E
+from paper_2505_06022_b200 import report, workloads as W
+from paper_2505_06022_b200.synergy import MeasuredKernel, select_measured
+from fakecq import FakeLib, LocalTransport
+
+
+def test_report_keys_and_identities(monkeypatch, tmp_path):
+    monkeypatch.setattr(N, "_lib", FakeLib(1, LocalTransport()))
+    prog = W.saxpy_program(64, kind="float64")
+    plan = cq.generate_commands(prog.graph(), 3)
+    res = E.run(plan)
+    rep = report.build_report(res)
+    assert list(rep) == ["makespan_s", "per_task", "per_device", "transfers"]
+    assert rep["transfers"] == {"count": len(plan.pushes()), "total_bytes": sum(p.bytes for p in plan.pushes())}
+    assert [t["id"] for t in rep["per_task"]] == [1]
+    assert set(rep["per_task"][0]["frequency_ghz_per_node"]) == {"0", "1", "2"}
+    report.write_outputs(res, tmp_path)
+    doc = json.loads((tmp_path / "buf_z.json").read_text())
+    assert doc["values"] == [2.0 * i + 1 for i in range(64)]
+    assert "traceEvents" in json.loads((tmp_path / "trace.json").read_text())
+
+
+def test_select_measured_follows_reference_rule():
+    k = MeasuredKernel("wave", {1000: (2.0, 100.0), 1500: (1.5, 120.0), 1965: (1.2, 150.0)})
+    assert select_measured(k, cq.EnergyTarget.MAX_PERF) == 1965
+    assert select_measured(k, cq.EnergyTarget.MIN_ENERGY) == 1000
+    # E*t: 200, 180, 180 -> tie goes to the higher clock
+    assert select_measured(k, cq.EnergyTarget.MIN_EDP) == 1965
+    # E*t^2: 400, 270, 216
+    assert select_measured(k, cq.EnergyTarget.MIN_ED2P) == 1965
+
+
+def test_select_measured_matches_model_selection_on_model_points():
+    """Fed the reference DeviceModel's own (t, E) per level, the measured
+    policy picks what the reference's select_frequency picks."""
+    from paper_2505_06022_b200.energy import _objective, exec_time
+    dev = cq.DeviceModel()
+    for beta in (0.0, 0.3, 1.0):
+        for t_ref in (Fraction(1, 1000), Fraction(3)):
+            pts = {}
+            for f in dev.levels_ghz:
+                t = exec_time(t_ref, beta, dev.f_ref_ghz, f)
+                pts[int(f * 1000)] = (t, dev._power_exact(f) * t)
+            k = MeasuredKernel("m", pts)
+            for target in cq.EnergyTarget:
+                want = cq.select_frequency(dev, target, t_ref, beta)
+                assert select_measured(k, target) == int(want * 1000)
