@@ -412,9 +412,16 @@ def bench_kernels(args, dist, placement, peaks):
 
 # ------------------------------------------------------------- CPU baselines
 
+def _all_host_threads():
+    """torchrun exports OMP_NUM_THREADS=1; the CPU arms use every core
+    (must be set before the OpenMP runtime of the oracle library loads)."""
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
+
+
 def cpu_wave_baseline(seconds=12.0, size=SIZE):
     """The CPU port of the wave step (oracle/cq_oracle.c, OpenMP over all
     host threads) on the same 16384^2 fp32 grid, bounded to ~``seconds``."""
+    _all_host_threads()
     from oracle import native as onat
     u = np.random.default_rng(2).uniform(0, 1, (size, size)).astype(np.float32)
     up = u.copy()
@@ -439,6 +446,7 @@ def reference_arm(args, dist):
     to the GPU box, so this times its C restatement (oracle/), all threads."""
     if dist.rank != 0:
         return None
+    _all_host_threads()
     from oracle import native as onat
     size = args.size
     u = np.random.default_rng(2).uniform(0, 1, (size, size)).astype(np.float32)

@@ -287,7 +287,21 @@ static int copy_box_generic(cudaStream_t st, int eb, char* dst, const cq_box_t& 
   char* d0 = dst + cell_offset(dalloc, dstride, p) * eb;
   const char* s0 = src + cell_offset(salloc, sstride, p) * eb;
   if (box_contiguous(box, dalloc) && box_contiguous(box, salloc)) {
-    CQ_CHECK_CUDA(cudaMemcpyAsync(d0, s0, n0 * n1 * n2 * eb, kind, st));
+    size_t bytes = (size_t)(n0 * n1 * n2 * eb);
+    cudaError_t e = cudaMemcpyAsync(d0, s0, bytes, kind, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      cudaPointerAttributes ad = {}, as = {};
+      cudaPointerGetAttributes(&ad, d0);
+      cudaGetLastError();
+      cudaPointerGetAttributes(&as, s0);
+      cudaGetLastError();
+      int cur = -1;
+      cudaGetDevice(&cur);
+      set_error("cudaMemcpyAsync(dst=%p type %d dev %d, src=%p type %d dev %d, %zu B, kind %d, cur dev %d): %s", d0,
+                (int)ad.type, ad.device, s0, (int)as.type, as.device, bytes, (int)kind, cur, cudaGetErrorString(e));
+      return CQ_ERR_CUDA;
+    }
     return CQ_OK;
   }
   if (n0 == 1) {

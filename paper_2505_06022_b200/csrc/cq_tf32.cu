@@ -107,6 +107,36 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// TMA load of one box into the same smem offset of every CTA in `mask`,
+// completing bytes on each destination CTA's mbarrier at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+// MMA completion -> arrive on the mbarrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -145,7 +175,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 
-template <int BN, int STAGES>
+// MC = CTAs per cluster along M sharing one B tile: each loads BN/MC rows of
+// B (hi and lo) and multicasts them to all MC CTAs, so per-CTA TMA traffic
+// per k block drops from 32*(BM+BN)*8 to 32*(BM+BN/MC)*8 bytes.
+template <int BN, int STAGES, int MC>
 __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
     sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                         const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -167,7 +200,7 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
     prefetch_map(&map_blo);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], 1);
+      mbar_init(&S.empty[s], MC);  // the stage is free once every consumer CTA is done
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.tfull[b], 1);
@@ -182,8 +215,12 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (MC > 1) cluster_sync();  // peers' barriers are initialised before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = S.tmem_base;
+  const uint32_t crank = MC > 1 ? cluster_rank() : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << MC) - 1);
+  constexpr int kBRows = BN / MC;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -195,8 +232,21 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
         const int kc = kb * BK;
         tma_load_2d(S.a_hi[s], &map_ahi, &S.full[s], kc, tile_m * BM);
         tma_load_2d(S.a_lo[s], &map_alo, &S.full[s], kc, tile_m * BM);
-        tma_load_2d(S.b_hi[s], &map_bhi, &S.full[s], kc, tile_n * BN);
-        tma_load_2d(S.b_lo[s], &map_blo, &S.full[s], kc, tile_n * BN);
+        if (MC == 1) {
+          tma_load_2d(S.b_hi[s], &map_bhi, &S.full[s], kc, tile_n * BN);
+          tma_load_2d(S.b_lo[s], &map_blo, &S.full[s], kc, tile_n * BN);
+        } else {
+          const int row = tile_n * BN + (int)crank * kBRows;
+          tma_load_2d_mc(S.b_hi[s] + crank * kBRows * BK, &map_bhi, &S.full[s], kc, row, kMask);
+          tma_load_2d_mc(S.b_lo[s] + crank * kBRows * BK, &map_blo, &S.full[s], kc, row, kMask);
+        }
+      }
+      if (MC > 1) {
+        // producer tail: every consumer arrive on this CTA's stage barriers
+        // has landed before the CTA may exit
+        for (int kb = num_kb; kb < num_kb + STAGES; ++kb) {
+          mbar_wait(&S.empty[kb % STAGES], ((kb / STAGES) & 1) ^ 1);
+        }
       }
     }
   } else if (warp == 1) {
@@ -224,7 +274,8 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
             mma_tf32(acc_addr, dah + o, dbl + o, idesc, 1);
             mma_tf32(acc_addr, dal + o, dbh + o, idesc, 1);
           }
-          mma_commit(&S.empty[s]);
+          if (MC == 1) mma_commit(&S.empty[s]);
+          else mma_commit_mc(&S.empty[s], kMask);
         }
         mma_commit(&S.tfull[buf]);
       }
@@ -271,6 +322,7 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (MC > 1) cluster_sync();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Epi<BN>::kTmemCols));
@@ -347,22 +399,35 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   return CQ_OK;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int MC>
 static int launch(cudaStream_t st, const float* ahi, const float* alo, const float* bhi, const float* blo, float* c,
                   int64_t ldc, int64_t m, int64_t n, int64_t k) {
   CUtensorMap ma, mal, mb, mbl;
   CQ_TRY(make_map(&ma, ahi, m, k, BM));
   CQ_TRY(make_map(&mal, alo, m, k, BM));
-  CQ_TRY(make_map(&mb, bhi, n, k, BN));
-  CQ_TRY(make_map(&mbl, blo, n, k, BN));
+  CQ_TRY(make_map(&mb, bhi, n, k, BN / MC));
+  CQ_TRY(make_map(&mbl, blo, n, k, BN / MC));
   size_t smem = sizeof(Smem<BN, STAGES>) + 1024;
-  auto kern = sgemm_3xtf32_kernel<BN, STAGES>;
+  auto kern = sgemm_3xtf32_kernel<BN, STAGES, MC>;
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((n + BN - 1) / BN), (unsigned)((m + BM - 1) / BM));
+  unsigned tiles_m = (unsigned)((m + BM - 1) / BM);
+  tiles_m = (tiles_m + MC - 1) / MC * MC;  // whole clusters; extra tiles load zeros, store nothing
+  dim3 grid((unsigned)((n + BN - 1) / BN), tiles_m);
   int group_kb = 4;  // K = 128 per TMEM accumulation group
   if (const char* g = getenv("CQ_TF32_GROUP_KB")) group_kb = atoi(g) > 0 ? atoi(g) : group_kb;
-  kern<<<grid, Epi<BN>::kThreads, smem, st>>>(ma, mal, mb, mbl, c, ldc, (int)m, (int)n, (int)k, group_kb);
-  CQ_CHECK_LAUNCH();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(Epi<BN>::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = MC;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CQ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mal, mb, mbl, c, ldc, (int)m, (int)n, (int)k, group_kb));
   return CQ_OK;
 }
 
@@ -387,9 +452,16 @@ int sgemm_3xtf32(cudaStream_t st, int sm_count, const float* a, int64_t lda, con
   tf32::split_transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(b, ldb, bhi, blo, k, n);
   CQ_CHECK_LAUNCH();
   const char* bn = getenv("CQ_TF32_BN");
+  const char* mc = getenv("CQ_TF32_MC");
   bool wide = n >= 256 && !(bn && atoi(bn) == 128);
-  int status = wide ? tf32::launch<256, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
-                    : tf32::launch<128, 3>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+  bool multicast = !(mc && atoi(mc) == 1);
+  int status;
+  if (wide)
+    status = multicast ? tf32::launch<256, 2, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
+                       : tf32::launch<256, 2, 1>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+  else
+    status = multicast ? tf32::launch<128, 3, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
+                       : tf32::launch<128, 3, 1>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
   cudaFreeAsync(scratch, st);
   return status;
 }

@@ -480,11 +480,18 @@ class Session:
                     touch.setdefault((c.node, buf), []).append(reg.bounding_box())
             elif isinstance(c, PushCommand):
                 bb = c.region.bounding_box()
-                touch.setdefault((c.src, c.buffer), []).append(bb)
+                if c.deps:
+                    # host-initialised pushes are uploaded at the destination,
+                    # so their source never holds the region on a device
+                    touch.setdefault((c.src, c.buffer), []).append(bb)
                 touch.setdefault((c.dst, c.buffer), []).append(bb)
         for name, entries in self.plan.final_locations.items():
-            for reg, _v, holders in entries:
-                touch.setdefault((min(holders), name), []).append(reg.bounding_box())
+            init = self.buffers[name].init.is_initialized
+            for reg, version, holders in entries:
+                if init and version == 1:
+                    continue  # gathered straight from the host array
+                for h in holders:
+                    touch.setdefault((h, name), []).append(reg.bounding_box())
         for (node, buf), boxes in sorted(touch.items()):
             if not self.local(node):
                 continue

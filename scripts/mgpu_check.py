@@ -63,14 +63,20 @@ def main():
     prog = W.nbody_program(nb, steps=2, pos=pos, vel=vel)
     res = E.run(cq.generate_commands(prog.graph(), world), placement=pl)
     if rank == 0:
+        # the j order is fixed independently of the GPU count, so the
+        # distributed result equals a 1-GPU run of the same program bit for bit
+        single = E.run(cq.generate_commands(prog.graph(), 1), placement=E.Placement(1, 0, (local,)))
+        ok = dsl.same_bits(res.buffers["P"], single.buffers["P"]) and \
+            dsl.same_bits(res.buffers["V"], single.buffers["V"])
         acc = onat.nbody_accel(pos, 0, nb, 1e-2)
-        p1 = pos[:, :3].astype(np.float64)
-        ok = np.isfinite(res.buffers["P"]).all() and np.isfinite(res.buffers["V"]).all()
-        # first kick is checked against the float64 oracle through the 2-step result
-        v1 = 1e-3 * acc
-        ok = ok and np.allclose(res.buffers["V"][:, :3], 2 * v1, rtol=5e-2, atol=1e-6)
-        check(f"nbody {nb} x2 steps all-gather", bool(ok))
-        np.save("/tmp/_nbody_mgpu.npy", res.buffers["P"])
+        # one kick from rest: V = dt * a within the SURVEY §8d tolerance
+        prog1 = W.nbody_program(nb, steps=1, pos=pos, vel=vel)
+        one = E.run(cq.generate_commands(prog1.graph(), world), placement=pl)
+        err = np.linalg.norm(one.buffers["V"][:, :3] / 1e-3 - acc, axis=1) / np.linalg.norm(acc, axis=1)
+        check(f"nbody {nb} x2 steps all-gather == 1 GPU; kick err {err.max():.1e}", ok and err.max() <= 1e-4)
+    else:
+        prog1 = W.nbody_program(nb, steps=1, pos=pos, vel=vel)
+        E.run(cq.generate_commands(prog1.graph(), world), placement=pl)
 
     # SGEMM slice mappers (A scatter + B broadcast), both variants
     m, nn, k = 512, 384, 256
