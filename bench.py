@@ -130,8 +130,10 @@ class Dist:
         if self.world > 1:
             import torch
             import torch.distributed as dist
+            import datetime
             torch.cuda.set_device(self.local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank),
+                                    timeout=datetime.timedelta(seconds=300))
             self.torch = torch
             self.dist = dist
 
@@ -222,7 +224,7 @@ def bench_wave(args, dist, placement, peaks):
     kern_ms = sum(sess.elapsed_ms(a, b) for _k, _c, _d, _s, a, b in dominant)
     kern_bytes = sum(12 * cells for _k, cells, *_ in dominant)
     sess.recycle()
-    energy = energy_loop(sess, 1.5) if args.energy else None
+    energy = energy_loop(sess, dist, dev_ms / args.steps, 1.5) if args.energy else None
     if energy and "j_per_iter" in energy:
         energy["j_per_time_step"] = energy["j_per_iter"] / steps
         energy["gb_per_joule"] = 12 * H * Wd * steps / 1e9 / energy["j_per_iter"] / world
@@ -311,20 +313,29 @@ def _timed_session(plan, placement, dist, reps, warm=2):
     return sess, dist.max(ms), per_kind, len(log)
 
 
-def energy_loop(sess, seconds=1.0):
-    """J per execute over >= ``seconds`` (NVML counter deltas)."""
+def energy_loop(sess, dist, ms_per_iter, seconds=1.0):
+    """J per execute over >= ``seconds`` (NVML counter deltas).  The
+    iteration count is agreed across ranks (every replay posts NCCL groups,
+    so all ranks must run the same number)."""
+    iters = int(dist.max(max(3, int(seconds * 1e3 / max(ms_per_iter, 1e-3)) + 1)))
+    dist.barrier()
     try:
         e0 = sess.energy_mj()
     except Exception as exc:  # noqa: BLE001
-        return {"error": str(exc)}
+        e0 = None
+        err = str(exc)
     t0 = time.perf_counter()
     n = 0
-    while time.perf_counter() - t0 < seconds or n < 3:
+    while n < iters:
         sess.execute(upload=False)
         n += 1
         if n % 4 == 0:
             sess.synchronize()
             sess.recycle()
+    if e0 is None:
+        sess.synchronize()
+        sess.recycle()
+        return {"error": err}
     sess.synchronize()
     sess.recycle()
     dt = time.perf_counter() - t0
@@ -373,7 +384,7 @@ def bench_kernels(args, dist, placement, peaks):
     inter = nb * nb * 3 * 3
     gflops = 20 * inter / (ms / 1e3) / 1e9
     kick_gflops = dist.min(20 * (kick[0] // 4) * nb / (kick[1] / 1e3) / 1e9)
-    energy = energy_loop(sess, 1.0) if args.energy else None
+    energy = energy_loop(sess, dist, ms / 3, 1.0) if args.energy else None
     clk = clocks.get("sm_mhz") or (energy or {}).get("sm_clock_mhz")
     out["nbody_262144"] = {"value": gflops, "unit": "GFLOP/s", "scaling": "strong",
                            "ms_per_step": ms / 9, "flop_per_interaction": 20,

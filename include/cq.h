@@ -109,6 +109,14 @@ int cq_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);
 int cq_stream_synchronize(int device, int stream);
 int cq_device_synchronize(int device);
 
+/* CUDA-graph capture of everything issued on the three streams of `device`
+ * between begin and end (kernels, copies, NCCL groups, event edges); the
+ * executable graph replays the whole plan with one launch. */
+int cq_graph_begin(int device);
+int cq_graph_end(int device, uint64_t* graph);
+int cq_graph_launch(uint64_t graph, int device);
+int cq_graph_destroy(uint64_t graph);
+
 /* ------------------------------------------------------------------- NCCL */
 int cq_nccl_unique_id(unsigned char id_out[128]);
 int cq_nccl_init(int device, int nranks, int rank, const unsigned char id[128]);

@@ -81,6 +81,10 @@ _SIGS = {
     "cq_event_elapsed_ms": (i32, [u64, u64, P(ctypes.c_float)]),
     "cq_stream_synchronize": (i32, [i32, i32]),
     "cq_device_synchronize": (i32, [i32]),
+    "cq_graph_begin": (i32, [i32]),
+    "cq_graph_end": (i32, [i32, P(u64)]),
+    "cq_graph_launch": (i32, [u64, i32]),
+    "cq_graph_destroy": (i32, [u64]),
     "cq_nccl_unique_id": (i32, [ctypes.c_char_p]),
     "cq_nccl_init": (i32, [i32, i32, i32, ctypes.c_char_p]),
     "cq_nccl_group_start": (i32, []),

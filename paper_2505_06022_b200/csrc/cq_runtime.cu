@@ -433,6 +433,58 @@ int cq_device_synchronize(int device) {
   return CQ_OK;
 }
 
+// ------------------------------------------------------------ graph capture
+// Fork: the compute stream starts a (relaxed-mode) capture and the boundary
+// and comm streams join it through an event; join: both record an event the
+// compute stream waits on before the capture ends.
+int cq_graph_begin(int device) {
+  CQ_STREAM(device, CQ_STREAM_COMPUTE);
+  cudaStream_t b = stream_of(device, CQ_STREAM_BOUNDARY), c = stream_of(device, CQ_STREAM_COMM);
+  CQ_CHECK_CUDA(cudaSetDevice(device));
+  CQ_CHECK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+  cudaEvent_t fork;
+  CQ_CHECK_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  CQ_CHECK_CUDA(cudaEventRecord(fork, st));
+  CQ_CHECK_CUDA(cudaStreamWaitEvent(b, fork, 0));
+  CQ_CHECK_CUDA(cudaStreamWaitEvent(c, fork, 0));
+  CQ_CHECK_CUDA(cudaEventDestroy(fork));
+  return CQ_OK;
+}
+
+int cq_graph_end(int device, uint64_t* graph) {
+  CQ_STREAM(device, CQ_STREAM_COMPUTE);
+  CQ_CHECK_CUDA(cudaSetDevice(device));
+  for (int s : {CQ_STREAM_BOUNDARY, CQ_STREAM_COMM}) {
+    cudaEvent_t join;
+    CQ_CHECK_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    CQ_CHECK_CUDA(cudaEventRecord(join, stream_of(device, s)));
+    CQ_CHECK_CUDA(cudaStreamWaitEvent(st, join, 0));
+    CQ_CHECK_CUDA(cudaEventDestroy(join));
+  }
+  cudaGraph_t g = nullptr;
+  CQ_CHECK_CUDA(cudaStreamEndCapture(st, &g));
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    set_error("cudaGraphInstantiate: %s", cudaGetErrorString(e));
+    return CQ_ERR_CUDA;
+  }
+  *graph = (uint64_t)(uintptr_t)exec;
+  return CQ_OK;
+}
+
+int cq_graph_launch(uint64_t graph, int device) {
+  CQ_STREAM(device, CQ_STREAM_COMPUTE);
+  CQ_CHECK_CUDA(cudaGraphLaunch((cudaGraphExec_t)(uintptr_t)graph, st));
+  return CQ_OK;
+}
+
+int cq_graph_destroy(uint64_t graph) {
+  CQ_CHECK_CUDA(cudaGraphExecDestroy((cudaGraphExec_t)(uintptr_t)graph));
+  return CQ_OK;
+}
+
 // -------------------------------------------------------------------- NCCL
 static ncclComm_t g_comm = nullptr;
 static int g_comm_device = -1;

@@ -948,6 +948,44 @@ class Session:
             elif self.local(step[1].node):
                 self.exec_command(step[1], step[2])
 
+    def capture(self):
+        """Capture one replay of the plan (``execute(upload=False)``) into a
+        CUDA graph -- kernels, copies, NCCL groups and the cross-stream event
+        edges -- so later replays cost one launch instead of one Python
+        dispatch per command.  One local device only (the one-rank-per-GPU
+        layout)."""
+        if len(self.devices) != 1:
+            raise ValidationError("graph capture needs exactly one local device")
+        d = self.devices[0]
+        self.synchronize()
+        self.recycle()
+        saved = self.want_trace
+        self.want_trace = False
+        N.call("cq_graph_begin", d)
+        handle = ctypes.c_uint64()
+        try:
+            self.execute(upload=False)
+        except Exception:
+            try:
+                N.call("cq_graph_end", d, ctypes.byref(handle))
+                N.call("cq_graph_destroy", handle)
+            except NativeError:
+                pass
+            self.want_trace = saved
+            raise
+        N.call("cq_graph_end", d, ctypes.byref(handle))
+        self.want_trace = saved
+        self.recycle()  # events recorded during capture are graph-internal
+        if getattr(self, "graph", None):
+            N.call("cq_graph_destroy", ctypes.c_uint64(self.graph))
+        self.graph = handle.value
+        return self.graph
+
+    def replay(self, times: int = 1):
+        """Launch the captured graph ``times`` times (asynchronous)."""
+        for _ in range(times):
+            N.call("cq_graph_launch", ctypes.c_uint64(self.graph), self.devices[0])
+
     def mark(self):
         """Join all streams of every local device and record a timing event
         per device on the compute stream; returns {device: event}."""
@@ -997,6 +1035,11 @@ class Session:
         self._t0 = {}
 
     def close(self):
+        if getattr(self, "graph", None):
+            for d in self.devices:
+                N.call("cq_stream_synchronize", d, N.STREAM_COMPUTE)
+            N.call("cq_graph_destroy", ctypes.c_uint64(self.graph))
+            self.graph = None
         self.release()
         for pool in self.free_events.values():
             for ev in pool:

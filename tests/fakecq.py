@@ -406,3 +406,56 @@ class GlooTransport:
         for addr, n, t in recvs:
             lib._mem(addr, n)[:] = t.numpy()
         lib.launches.append(("group", len(ops)))
+
+
+def _graph_api(cls):
+    """Graph capture in the double: record the issued calls and re-issue
+    them on launch (enough to exercise Session.capture/replay on CPU)."""
+    def begin(self, d):
+        self.capturing = []
+        return 0
+
+    def end(self, d, p):
+        self.graphs = getattr(self, "graphs", [])
+        self.graphs.append(self.capturing)
+        self.capturing = None
+        _obj(p).value = len(self.graphs)
+        return 0
+
+    def launch(self, g, d):
+        for name, args in self.graphs[_val(g) - 1]:
+            getattr(cls, name)(self, *args)
+        return 0
+
+    def destroy(self, g):
+        return 0
+    cls.cq_graph_begin, cls.cq_graph_end = begin, end
+    cls.cq_graph_launch, cls.cq_graph_destroy = launch, destroy
+    # wrap kernel entry points so they are recorded while capturing
+    for name in ("cq_saxpy", "cq_wave5", "cq_expr_eval", "cq_fill", "cq_copy_box", "cq_pack_box",
+                 "cq_unpack_box", "cq_nbody_kick", "cq_nbody_drift", "cq_sgemm"):
+        fn = getattr(cls, name)
+
+        def wrapped(self, *args, _fn=fn, _name=name):
+            if getattr(self, "capturing", None) is not None:
+                self.capturing.append((_name, _copy_args(args)))
+                return 0
+            return _fn(self, *args)
+        setattr(cls, name, wrapped)
+    return cls
+
+
+def _copy_args(args):
+    out = []
+    for a in args:
+        o = _obj(a)
+        if isinstance(o, ctypes.Structure):
+            c = type(o)()
+            ctypes.pointer(c)[0] = o
+            out.append(c)
+        else:
+            out.append(_val(a))
+    return out
+
+
+_graph_api(FakeLib)

@@ -148,3 +148,21 @@ def test_two_ranks_gloo(tmp_path):
         if key.startswith("g"):
             idx, name = key[1:].split("__")
             assert dsl.same_bits(val, EXPECTED[f"p{idx}__{name}"]), key
+
+
+def test_graph_capture_replays_same_commands(fake):
+    lib = fake(1)
+    h, w = 40, 32
+    u0 = np.random.default_rng(4).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=4, kind="float32", u0=u0, up0=u0)
+    plan = cq.generate_commands(prog.graph(), 3)
+    s = E.Session(plan, E.Placement(1, 0, (0,)))
+    s.execute(upload=True)
+    s.synchronize()
+    base = lib.launches.count("wave5")
+    s.capture()
+    assert lib.launches.count("wave5") == base  # capture records, runs nothing
+    s.replay(2)
+    s.synchronize()
+    assert lib.launches.count("wave5") == 3 * base
+    s.close()

@@ -202,3 +202,28 @@ def test_sgemm_baseline_size_sampled(variant):
     c, cabs = onat.sgemm_rows(a, b, rows)
     err = np.abs(res.buffers["C"][rows] - c) / cabs
     assert err.max() <= 1e-6, err.max()
+
+
+@pytest.mark.parametrize("nodes", [1, 3])
+def test_graph_replay_equals_plain_replay(nodes):
+    from paper_2505_06022_b200.executor import Placement, Session
+    h, w = 256, 384
+    u0 = np.random.default_rng(8).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=6, kind="float32", u0=u0, up0=u0)
+    plan = cq.generate_commands(prog.graph(), nodes)
+    out = []
+    for graph in (False, True):
+        s = Session(plan, Placement(1, 0, (0,)))
+        s.execute(upload=True)
+        s.synchronize()
+        s.recycle()
+        if graph:
+            s.capture()
+            s.replay(3)
+        else:
+            for _ in range(3):
+                s.execute(upload=False)
+        s.synchronize()
+        out.append(s.results())
+        s.close()
+    assert dsl.same_bits(out[0]["u"], out[1]["u"]) and dsl.same_bits(out[0]["up"], out[1]["up"])
