@@ -202,27 +202,53 @@ def bench_wave(args, dist, placement, peaks):
     sess.execute(upload=True)
     sess.synchronize()
     sess.recycle()
-    for _ in range(args.warmup):
-        sess.execute(upload=False)
-        sess.synchronize()
-        sess.recycle()
-    dist.barrier()
-    dev = placement.devices[0]
-    with ClockSampler(dev) as clocks:
-        m0 = sess.mark()
-        for _ in range(args.steps):
-            sess.execute(upload=False)
-        m1 = sess.mark()
-        sess.synchronize()
-    dev_ms = max(sess.elapsed_ms(m0[d], m1[d]) for d in sess.devices)
+    # one traced replay: per-launch CUDA-event times of every kernel
+    sess.execute(upload=False)
+    sess.synchronize()
     wave_launches = [x for x in sess.launch_log if x[0] == "wave5"]
-    gpu_launches = len(sess.launch_log)
+    launches_per_replay = len(sess.launch_log)
     # dominant launches only: at N > 1 the halo-row launches run concurrently
     # on the boundary stream, so summing every launch would double-count time
     dom_launch = max(wave_launches, key=lambda x: x[1])
     dominant = [x for x in wave_launches if x[1] == dom_launch[1]]
     kern_ms = sum(sess.elapsed_ms(a, b) for _k, _c, _d, _s, a, b in dominant)
     kern_bytes = sum(12 * cells for _k, cells, *_ in dominant)
+    sess.recycle()
+    # the timed replays run as one CUDA graph per rank (kernels, copies and
+    # NCCL groups captured once), so no per-command host dispatch remains
+    replay_mode = "cuda_graph"
+    if args.no_graph:
+        replay_mode = "stream"
+    else:
+        try:
+            sess.capture()
+        except Exception as exc:  # noqa: BLE001
+            replay_mode = f"stream (graph capture failed: {exc})"[:200]
+            sess.synchronize()
+            sess.recycle()
+    graph = replay_mode == "cuda_graph"
+
+    def replay_once():
+        if graph:
+            sess.replay(1)
+        else:
+            sess.execute(upload=False)
+
+    for _ in range(args.warmup):
+        replay_once()
+        sess.synchronize()
+        if not graph:
+            sess.recycle()
+    dist.barrier()
+    dev = placement.devices[0]
+    with ClockSampler(dev) as clocks:
+        m0 = sess.mark()
+        for _ in range(args.steps):
+            replay_once()
+        m1 = sess.mark()
+        sess.synchronize()
+    dev_ms = max(sess.elapsed_ms(m0[d], m1[d]) for d in sess.devices)
+    gpu_launches = launches_per_replay * args.steps
     sess.recycle()
     energy = energy_loop(sess, dist, dev_ms / args.steps, 1.5) if args.energy else None
     if energy and "j_per_iter" in energy:
@@ -276,6 +302,7 @@ def bench_wave(args, dist, placement, peaks):
                      "peak_source": peaks[1] + " hbm_gbs (torch copy)"},
         "clocks": clk,
         "gpu_launches": gpu_launches,
+        "replay": replay_mode,
         "energy": energy,
         "H": H, "W": Wd,
     }
@@ -293,24 +320,39 @@ def _timed_session(plan, placement, dist, reps, warm=2):
         sess.execute(upload=False)
         sess.synchronize()
         sess.recycle()
-    dist.barrier()
-    with ClockSampler(placement.devices[0]) as clocks:
-        m0 = sess.mark()
-        for _ in range(reps):
-            sess.execute(upload=False)
-        m1 = sess.mark()
-        sess.synchronize()
-    sess.clocks = clocks.summary()
-    ms = max(sess.elapsed_ms(m0[d], m1[d]) for d in sess.devices)
-    log = list(sess.launch_log)
+    # traced replay: per-kernel CUDA-event times
+    sess.execute(upload=False)
+    sess.synchronize()
+    log = [(k, c * reps, d, s, a, b) for k, c, d, s, a, b in sess.launch_log]
     per_kind = {}
     for kind, cells, _d, _s, a, b in log:
         k = per_kind.setdefault(kind, [0, 0.0, 0])
         k[0] += cells
-        k[1] += sess.elapsed_ms(a, b)
-        k[2] += 1
+        k[1] += sess.elapsed_ms(a, b) * reps
+        k[2] += reps
     sess.recycle()
-    return sess, dist.max(ms), per_kind, len(log)
+    graph = True
+    try:
+        sess.capture()
+    except Exception:  # noqa: BLE001
+        graph = False
+        sess.synchronize()
+        sess.recycle()
+    dist.barrier()
+    with ClockSampler(placement.devices[0]) as clocks:
+        m0 = sess.mark()
+        for _ in range(reps):
+            if graph:
+                sess.replay(1)
+            else:
+                sess.execute(upload=False)
+        m1 = sess.mark()
+        sess.synchronize()
+    sess.clocks = clocks.summary()
+    sess.clocks["replay"] = "cuda_graph" if graph else "stream"
+    ms = max(sess.elapsed_ms(m0[d], m1[d]) for d in sess.devices)
+    sess.recycle()
+    return sess, dist.max(ms), per_kind, len(log) * reps
 
 
 def energy_loop(sess, dist, ms_per_iter, seconds=1.0):
@@ -327,7 +369,10 @@ def energy_loop(sess, dist, ms_per_iter, seconds=1.0):
     t0 = time.perf_counter()
     n = 0
     while n < iters:
-        sess.execute(upload=False)
+        if getattr(sess, "graph", None):
+            sess.replay(1)
+        else:
+            sess.execute(upload=False)
         n += 1
         if n % 4 == 0:
             sess.synchronize()
@@ -506,6 +551,7 @@ def main():
     ap.add_argument("--no-kernels", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-energy", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="replay via per-command stream dispatch")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     args.sgemm_variants = [v for v in args.sgemm_variants.split(",") if v]
@@ -545,7 +591,8 @@ def main():
                                    f"bench step, neighborhood(1,1) halo exchange",
                        "parallelism": f"dp{dist.world} (row slabs, one rank per GPU)",
                        "l2": "inputs 2 GiB/GPU >> 126 MB L2 (no flush needed)",
-                       "plan_s": wave["plan_s"], "init": "Gaussian pulse (SURVEY.md §8d)"},
+                       "plan_s": wave["plan_s"], "init": "Gaussian pulse (SURVEY.md §8d)",
+                       "replay": wave["replay"]},
             "e2e": wave["e2e"], "roofline": wave["roofline"], "cpu_baseline": cpu,
             "clocks": wave["clocks"], "gpu_launches": wave["gpu_launches"],
             "energy": {"wave5": wave["energy"],

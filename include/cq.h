@@ -199,6 +199,15 @@ enum { CQ_SGEMM_FFMA = 0, CQ_SGEMM_3XTF32 = 1 };
 int cq_sgemm(int device, int stream, int variant, const float* a, int64_t lda, const float* b,
              int64_t ldb, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k);
 
+/* ---------------------------------------------------------------- planner */
+/* Native generate_commands (reference scheduler.py:224-369, region algebra
+ * region.py:113-170): host-only, no GPU needed.  `program` / `*out` use the
+ * int64 wire format documented in csrc/cq_plan.cpp; free *out with
+ * cq_plan_free. */
+int cq_plan_generate(const int64_t* program, int64_t length, int node_count, int64_t** out,
+                     int64_t* out_length);
+int cq_plan_free(int64_t* out);
+
 /* ------------------------------------------------------------------- NVML */
 int cq_nvml_init(void);
 int cq_nvml_energy_mj(int device, uint64_t* mj);

@@ -103,6 +103,8 @@ _SIGS = {
     "cq_nbody_kick": (i32, [i32, i32, vp, i64, vp, vp, i64, i64, ctypes.c_float, ctypes.c_float]),
     "cq_nbody_drift": (i32, [i32, i32, vp, vp, vp, i64, ctypes.c_float]),
     "cq_sgemm": (i32, [i32, i32, i32, vp, i64, vp, i64, vp, i64, i64, i64, i64]),
+    "cq_plan_generate": (i32, [P(i64), i64, i32, P(P(i64)), P(i64)]),
+    "cq_plan_free": (i32, [P(i64)]),
     "cq_nvml_init": (i32, []),
     "cq_nvml_energy_mj": (i32, [i32, P(u64)]),
     "cq_nvml_power_mw": (i32, [i32, P(ctypes.c_uint)]),
@@ -133,6 +135,25 @@ def load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+_host_lib = None
+
+
+def load_host():
+    """The real libcq for host-only entry points (the planner): never the
+    device-side test double a CPU test may install as ``_lib``."""
+    global _host_lib
+    if _host_lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"libcq.so not found at {LIB_PATH}")
+        lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+        for name in ("cq_plan_generate", "cq_plan_free", "cq_last_error"):
+            res, args = _SIGS[name]
+            getattr(lib, name).restype = res
+            getattr(lib, name).argtypes = args
+        _host_lib = lib
+    return _host_lib
 
 
 def check(status, what=""):

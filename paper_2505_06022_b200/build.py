@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libcq.so")
-SOURCES = ["cq_runtime.cu", "cq_kernels.cu", "cq_sgemm.cu", "cq_tf32.cu", "cq_nvml.cu"]
+SOURCES = ["cq_runtime.cu", "cq_kernels.cu", "cq_sgemm.cu", "cq_tf32.cu", "cq_nvml.cu", "cq_plan.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -52,6 +52,14 @@ int ensure_device(int device) {
   CQ_CHECK_CUDA(cudaMalloc(&d.error_flag, 8 * sizeof(int)));
   // error key all-ones == "no error" (atomicMin records the first failure)
   CQ_CHECK_CUDA(cudaMemset(d.error_flag, 0xff, 2 * sizeof(int)));
+  // stream-ordered scratch (cudaMallocAsync in the GEMM split pass) keeps its
+  // physical memory between replays instead of re-mapping it every call
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
   cudaDeviceProp prop;
   CQ_CHECK_CUDA(cudaGetDeviceProperties(&prop, device));
   d.sm_count = prop.multiProcessorCount;
