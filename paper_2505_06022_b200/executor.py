@@ -897,21 +897,32 @@ class Session:
         on every rank; computed once per session)."""
         if self._sched is not None:
             return self._sched
+        # Task-major order: every push of a task depends only on commands of
+        # earlier tasks (producers are read from the table state before the
+        # task, scheduler.py:263-314), so all of a task's pushes can be posted
+        # as ONE group before any of its executes.  That order is topological
+        # -- awaits precede the executes that need them and same-task hazard
+        # pushes precede the overwriting execute -- and it turns the plan's
+        # per-destination push runs (e.g. an all-gather) into one NCCL group.
+        segments = []
+        pushes, execs, pending, cur = [], [], [], None
+        for c in self.plan.commands:
+            if isinstance(c, PushCommand):
+                pending.append(c)
+            elif isinstance(c, ExecuteCommand):
+                if cur is not None and c.task_id != cur:
+                    segments.append((pushes, execs))
+                    pushes, execs = [], []
+                cur = c.task_id
+                pushes.extend(pending)
+                pending = []
+                execs.append(c)
+        if execs or pending:
+            segments.append((pushes + pending, execs))
         steps = []   # ("group", [push...]) | ("exec", cmd, awaited)
-        group, group_acc = [], []
-        for cid in kahn_order(self.plan):
-            c = self.by_id[cid]
-            if isinstance(c, ExecuteCommand):
-                if group:
-                    steps.append(("group", group))
-                group, group_acc = [], []
-                aw = {}
-                for d in c.deps:
-                    a = self.by_id[d]
-                    if isinstance(a, AwaitPushCommand) and a.dst == c.node:
-                        aw[a.buffer] = aw[a.buffer].union(a.region) if a.buffer in aw else a.region
-                steps.append(("exec", c, aw))
-            elif isinstance(c, PushCommand):
+        for seg_pushes, seg_execs in segments:
+            group, group_acc = [], []
+            for c in seg_pushes:
                 acc = [(c.src, c.buffer, c.region, False), (c.dst, c.buffer, c.region, True)]
                 if any(n == n2 and b == b2 and (w or w2) and r.overlaps(r2)
                        for n, b, r, w in acc for n2, b2, r2, w2 in group_acc):
@@ -919,9 +930,15 @@ class Session:
                     group, group_acc = [], []
                 group.append(c)
                 group_acc.extend(acc)
-            # AwaitPush: its receive is posted with the push (same group)
-        if group:
-            steps.append(("group", group))
+            if group:
+                steps.append(("group", group))
+            for c in seg_execs:
+                aw = {}
+                for d in c.deps:
+                    a = self.by_id[d]
+                    if isinstance(a, AwaitPushCommand) and a.dst == c.node:
+                        aw[a.buffer] = aw[a.buffer].union(a.region) if a.buffer in aw else a.region
+                steps.append(("exec", c, aw))
         self._sched = steps
         return steps
 
