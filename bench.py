@@ -172,12 +172,15 @@ def wave_inputs(h, w, rows):
     from paper_2505_06022_b200.region import Box
     box = Box((rows[0], 0), (rows[1], w))
     u0 = E.pinned_empty((h, w), np.float32, box)
-    i = np.arange(rows[0], rows[1], dtype=np.float64)[:, None] - h / 2
-    j = np.arange(w, dtype=np.float64)[None, :] - w / 2
-    s = (w / 16.0) ** 2
-    u0[rows[0]:rows[1]] = np.exp(-(i * i + j * j) / (2 * s)).astype(np.float32)
     up0 = E.pinned_empty((h, w), np.float32, box)
-    up0[rows[0]:rows[1]] = u0[rows[0]:rows[1]]
+    j = np.arange(w, dtype=np.float64)[None, :] - w / 2
+    jj = j * j
+    s2 = 2 * (w / 16.0) ** 2
+    for r0 in range(rows[0], rows[1], 1024):  # row blocks keep host temporaries small
+        r1 = min(r0 + 1024, rows[1])
+        i = np.arange(r0, r1, dtype=np.float64)[:, None] - h / 2
+        u0[r0:r1] = np.exp(-(i * i + jj) / s2).astype(np.float32)
+        up0[r0:r1] = u0[r0:r1]
     return u0, up0
 
 
@@ -554,7 +557,7 @@ def main():
     ap.add_argument("--wave-steps", type=int, default=WAVE_STEPS)
     ap.add_argument("--nbody", type=int, default=262144)
     ap.add_argument("--sgemm", type=int, default=16384)
-    ap.add_argument("--sgemm-variants", default="ffma")
+    ap.add_argument("--sgemm-variants", default="3xtf32,ffma")
     ap.add_argument("--no-kernels", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-energy", action="store_true")

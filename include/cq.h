@@ -179,6 +179,12 @@ typedef struct {
   cq_box_t view_check[CQ_EXPR_MAX_VIEWS][CQ_EXPR_MAX_CHECK_BOXES];
 } cq_expr_t;
 int cq_expr_eval(int device, int stream, const cq_expr_t* expr);
+/* DSL -> CUDA JIT: compile straight-line CUDA for a body with NVRTC (sm_100a)
+ * and launch it on the same cq_expr_t block (bit-identical to cq_expr_eval).
+ * `headers` are in-memory include files (cq.h itself). */
+int cq_jit_compile(const char* source, const char* kernel_name, int n_headers, const char** header_src,
+                   const char** header_names, uint64_t* handle);
+int cq_jit_launch(uint64_t handle, int device, int stream, const cq_expr_t* expr);
 /* Sticky per-device error flag written by cq_expr_eval: code 0 / CQ_ERR_EVAL /
  * CQ_ERR_MAPPER with the first failing cell (row-major minimum). */
 int cq_error_flag(int device, int* code, int64_t point[CQ_MAX_DIMS], int clear);

@@ -103,6 +103,9 @@ _SIGS = {
     "cq_nbody_kick": (i32, [i32, i32, vp, i64, vp, vp, i64, i64, ctypes.c_float, ctypes.c_float]),
     "cq_nbody_drift": (i32, [i32, i32, vp, vp, vp, i64, ctypes.c_float]),
     "cq_sgemm": (i32, [i32, i32, i32, vp, i64, vp, i64, vp, i64, i64, i64, i64]),
+    "cq_jit_compile": (i32, [ctypes.c_char_p, ctypes.c_char_p, i32, P(ctypes.c_char_p),
+                             P(ctypes.c_char_p), P(u64)]),
+    "cq_jit_launch": (i32, [u64, i32, i32, P(CqExpr)]),
     "cq_plan_generate": (i32, [P(i64), i64, i32, P(P(i64)), P(i64)]),
     "cq_plan_free": (i32, [P(i64)]),
     "cq_nvml_init": (i32, []),
@@ -148,7 +151,7 @@ def load_host():
         if not os.path.exists(LIB_PATH):
             raise NativeError(f"libcq.so not found at {LIB_PATH}")
         lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
-        for name in ("cq_plan_generate", "cq_plan_free", "cq_last_error"):
+        for name in ("cq_plan_generate", "cq_plan_free", "cq_last_error", "cq_jit_compile"):
             res, args = _SIGS[name]
             getattr(lib, name).restype = res
             getattr(lib, name).argtypes = args

@@ -14,7 +14,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libcq.so")
-SOURCES = ["cq_runtime.cu", "cq_kernels.cu", "cq_sgemm.cu", "cq_tf32.cu", "cq_nvml.cu", "cq_plan.cpp"]
+SOURCES = ["cq_runtime.cu", "cq_kernels.cu", "cq_sgemm.cu", "cq_tf32.cu", "cq_nvml.cu", "cq_plan.cpp",
+           "cq_jit.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -61,8 +62,8 @@ def build(force=False, verbose=False) -> str:
                 print("compiled", os.path.relpath(s, ROOT))
     objs = [os.path.join(OBJ, s + ".o") for s in SOURCES]
     if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-ldl",
-               "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-lnvrtc", "-ldl",
+               "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu:/usr/local/cuda/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

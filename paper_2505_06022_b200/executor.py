@@ -40,6 +40,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native as N
+from . import jit
 from .errors import EvalError, MapperViolationError, NativeError, ValidationError
 from .lowering import bind_task
 from .model import AccessMode, NativeKernel, apply_mapper
@@ -889,6 +890,14 @@ class Session:
                     X.view_check[vi][0] = N.box3((0,) * b.dims, (0,) * b.dims)
                 for bi, rb in enumerate(region.boxes):
                     X.view_check[vi][bi] = _cbox(rb)
+        needs_check = any(X.view_n_check[vi] for vi in range(X.n_views))
+        if not needs_check and jit.enabled_for(box.volume()):
+            # compiled straight-line kernel (same parameter block, same bits)
+            outs = [list(zip(code_ops[X.out_code_begin[o]:X.out_code_end[o]],
+                             code_args[X.out_code_begin[o]:X.out_code_end[o]])) for o in range(X.n_out)]
+            h = jit.handle_for(X.kind, task.dims, outs, slots, [X.view_dims[i] for i in range(X.n_views)])
+            N.call("cq_jit_launch", ctypes.c_uint64(h), dev, stream, ctypes.byref(X))
+            return
         N.call("cq_expr_eval", dev, stream, ctypes.byref(X))
 
     # ---- the walk --------------------------------------------------------

@@ -330,6 +330,19 @@ class FakeLib:
         self.launches.append("expr")
         return 0
 
+    def cq_jit_compile(self, *args):
+        # real NVRTC compile of the generated kernel (host-only, no GPU);
+        # the double then runs the body through its interpreter
+        self.jit_compiled = getattr(self, "jit_compiled", 0) + 1
+        status = N.load_host().cq_jit_compile(*args)
+        if status:
+            self.err = N.load_host().cq_last_error()
+        return status
+
+    def cq_jit_launch(self, h, d, s, X):
+        self.launches.append("jit")
+        return self.cq_expr_eval(d, s, X)
+
     def cq_error_flag(self, d, code, pt, clear):
         _obj(code).value = self.flag or 0
         if clear:
