@@ -623,15 +623,38 @@ int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const flo
                   float* vel, int64_t i_lo, int64_t i_hi, float eps2, float dt) {
   CQ_GET_STREAM(device, stream);
   if (i_hi <= i_lo) return CQ_OK;
-  static int np = [] {
+  static int forced = [] {
     const char* e = getenv("CQ_NBODY_NP");
-    return e ? atoi(e) : 4;  // measured on B200: NP=4 67.2%, 2 64.5%, 1 62.7% of FP32 peak
+    return e ? atoi(e) : 0;
   }();
   const int64_t bodies = i_hi - i_lo;
-  // fewer i-bodies per GPU (many GPUs): halve the pairs per lane until the
-  // grid has >= 4 blocks per SM, so every SM stays busy
-  int use = np;
-  while (use > 1 && bodies < (int64_t)ds->sm_count * 4 * 64 * use) use = use > 2 ? 2 : 1;
+  int use = forced;
+  if (use == 0) {
+    // pick the pairs-per-lane variant with the best expected rate: its
+    // steady-state efficiency (measured on B200 with many waves: NP=4 67.2%,
+    // NP=2 64.5%, NP=1 62.7% of FP32 peak) times the fill of its last wave
+    // (blocks / (SMs x resident blocks per SM), rounded up).  Per-body
+    // results do not depend on NP, so this never changes the bits.
+    static int res[5] = {0, 0, 0, 0, 0};
+    if (!res[1]) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], nbody_kick_kernel<1>, NB_WARPS * 32, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], nbody_kick_kernel<2>, NB_WARPS * 32, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[4], nbody_kick_kernel<4>, NB_WARPS * 32, 0);
+    }
+    const double base[5] = {0, 0.627, 0.645, 0, 0.672};
+    double best = -1.0;
+    for (int p : {4, 2, 1}) {
+      double blocks = (double)((bodies + 64 * p - 1) / (64 * p));
+      double slots = (double)ds->sm_count * (res[p] > 0 ? res[p] : 1);
+      double waves = blocks / slots;
+      double fill = waves / ceil(waves);
+      double eff = base[p] * fill;
+      if (eff > best + 1e-9) {
+        best = eff;
+        use = p;
+      }
+    }
+  }
   switch (use) {
 #define NB_LAUNCH(P)                                                                                     \
   case P:                                                                                              \
