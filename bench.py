@@ -422,6 +422,32 @@ def bench_kernels(args, dist, placement, peaks):
                       "note": "2^24 x fp32 (192 MiB) fits in L2" if n == 1 << 24 else "inputs > L2"}
         sess.close()
 
+    # wave variants: float64 (the reference's own element kind, 24 B/cell/step,
+    # weak: 16384^2 per GPU) and strong scaling (global 16384^2 over N GPUs, fp32)
+    for label, kind, rows, esize in (("wave_f64_weak", "float64", args.size * world, 24),
+                                     ("wave_f32_strong", "float32", args.size, 12)):
+        steps = 20
+        z = np.zeros((1, 1))
+        from paper_2505_06022_b200.model import Buffer, BufferInit
+        from paper_2505_06022_b200.region import Box
+        ext = Box.from_shape((rows, args.size))
+        bufs = {"u": Buffer("u", ext, kind, BufferInit.constant(0.5)),
+                "up": Buffer("up", ext, kind, BufferInit.constant(0.25))}
+        tasks = [W.wave_task(s, rows, args.size, C) for s in range(steps)]
+        g = cq.TaskGraph(bufs)
+        for t in tasks:
+            g.submit(t)
+        del z
+        plan = cq.generate_commands(g, world)
+        sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=3, warm=1)
+        wk = kinds.get("wave5", [0, 1.0, 1])
+        value = esize * rows * args.size * steps * 3 / (ms / 1e3) / 1e9
+        out[label] = {"value": value, "unit": "GB/s", "scaling": "weak" if "weak" in label else "strong",
+                      "bytes_per_cell": esize, "time_steps": steps, "ms_per_time_step": ms / 3 / steps,
+                      "kernel_gbs_min_rank": dist.min(esize * wk[0] / (wk[1] / 1e3) / 1e9),
+                      "clocks": sess.clocks}
+        sess.close()
+
     # N-body: 262144 bodies, 'all' mapper all-gather each step
     nb = args.nbody
     prog = W.nbody_program(nb, steps=3)

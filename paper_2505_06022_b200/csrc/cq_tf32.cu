@@ -30,7 +30,9 @@ namespace cq {
 namespace tf32 {
 
 constexpr int BM = 128;
-constexpr int BK = 32;  // fp32 elements = 128 bytes = one swizzle atom row
+// BK (fp32 per k block) is a template parameter: 32 -> 128-byte swizzle
+// atoms (one row = one k block), 16 -> 64-byte atoms (half-size stages,
+// twice as many in flight).
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -72,14 +74,15 @@ __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
 
 // K-major operand tile, 128-byte swizzle: rows of 128 B, 8-row groups 1024 B
 // apart (SBO), LBO unused for swizzled K-major; descriptor version 1 (sm_100).
+template <int BK>
 __device__ __forceinline__ uint64_t smem_desc(const void* tile) {
   uint64_t addr = smem_u32(tile);
   uint64_t d = 0;
   d |= (addr & 0x3FFFFull) >> 4;          // start address      [0,14)
   d |= (uint64_t)1 << 16;                  // LBO (ignored)      [16,30)
-  d |= (uint64_t)(1024 >> 4) << 32;        // SBO = 1024 B       [32,46)
+  d |= (uint64_t)((8 * BK * 4) >> 4) << 32; // SBO: 8-row group  [32,46)
   d |= (uint64_t)1 << 46;                  // version            [46,48)
-  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B       [61,64)
+  d |= (uint64_t)(BK == 32 ? 2 : 4) << 61; // SWIZZLE_128B / 64B [61,64)
   return d;
 }
 
@@ -153,7 +156,7 @@ struct Epi {
   static constexpr uint32_t kTmemCols = 2 * BN;  // double-buffered accumulator
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int BK>
 struct Smem {
   float a_hi[STAGES][BM * BK];
   float a_lo[STAGES][BM * BK];
@@ -178,14 +181,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // MC = CTAs per cluster along M sharing one B tile: each loads BN/MC rows of
 // B (hi and lo) and multicasts them to all MC CTAs, so per-CTA TMA traffic
 // per k block drops from 32*(BM+BN)*8 to 32*(BM+BN/MC)*8 bytes.
-template <int BN, int STAGES, int MC>
+template <int BN, int STAGES, int MC, int BK>
 __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
     sgemm_3xtf32_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                         const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                         float* __restrict__ C, int64_t ldc, int m, int n, int k, int group_kb) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128-byte swizzle atoms
-  Smem<BN, STAGES>& S = *reinterpret_cast<Smem<BN, STAGES>*>(
+  Smem<BN, STAGES, BK>& S = *reinterpret_cast<Smem<BN, STAGES, BK>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile_n = blockIdx.x, tile_m = blockIdx.y;
@@ -264,8 +267,8 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
           const uint32_t phase = (kb / STAGES) & 1;
           mbar_wait(&S.full[s], phase);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint64_t dah = smem_desc(S.a_hi[s]), dal = smem_desc(S.a_lo[s]);
-          const uint64_t dbh = smem_desc(S.b_hi[s]), dbl = smem_desc(S.b_lo[s]);
+          const uint64_t dah = smem_desc<BK>(S.a_hi[s]), dal = smem_desc<BK>(S.a_lo[s]);
+          const uint64_t dbh = smem_desc<BK>(S.b_hi[s]), dbl = smem_desc<BK>(S.b_lo[s]);
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             // advance 8 fp32 = 32 bytes inside the swizzle atom: +2 in addr>>4
@@ -378,8 +381,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2-D row-major fp32 [rows, cols] (cols contiguous), box = [BK cols, box_rows].
-static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows) {
+// 2-D row-major fp32 [rows, cols] (cols contiguous), box = [bk cols, box_rows].
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows, int bk) {
   auto encode = get_encode();
   if (!encode) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -387,10 +390,10 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -399,21 +402,21 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   return CQ_OK;
 }
 
-template <int BN, int STAGES, int MC>
+template <int BN, int STAGES, int MC, int BK>
 static int launch(cudaStream_t st, const float* ahi, const float* alo, const float* bhi, const float* blo, float* c,
                   int64_t ldc, int64_t m, int64_t n, int64_t k) {
   CUtensorMap ma, mal, mb, mbl;
-  CQ_TRY(make_map(&ma, ahi, m, k, BM));
-  CQ_TRY(make_map(&mal, alo, m, k, BM));
-  CQ_TRY(make_map(&mb, bhi, n, k, BN / MC));
-  CQ_TRY(make_map(&mbl, blo, n, k, BN / MC));
-  size_t smem = sizeof(Smem<BN, STAGES>) + 1024;
-  auto kern = sgemm_3xtf32_kernel<BN, STAGES, MC>;
+  CQ_TRY(make_map(&ma, ahi, m, k, BM, BK));
+  CQ_TRY(make_map(&mal, alo, m, k, BM, BK));
+  CQ_TRY(make_map(&mb, bhi, n, k, BN / MC, BK));
+  CQ_TRY(make_map(&mbl, blo, n, k, BN / MC, BK));
+  size_t smem = sizeof(Smem<BN, STAGES, BK>) + 1024;
+  auto kern = sgemm_3xtf32_kernel<BN, STAGES, MC, BK>;
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   unsigned tiles_m = (unsigned)((m + BM - 1) / BM);
   tiles_m = (tiles_m + MC - 1) / MC * MC;  // whole clusters; extra tiles load zeros, store nothing
   dim3 grid((unsigned)((n + BN - 1) / BN), tiles_m);
-  int group_kb = 4;  // K = 128 per TMEM accumulation group
+  int group_kb = 128 / BK;  // K = 128 per TMEM accumulation group
   if (const char* g = getenv("CQ_TF32_GROUP_KB")) group_kb = atoi(g) > 0 ? atoi(g) : group_kb;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -453,15 +456,20 @@ int sgemm_3xtf32(cudaStream_t st, int sm_count, const float* a, int64_t lda, con
   CQ_CHECK_LAUNCH();
   const char* bn = getenv("CQ_TF32_BN");
   const char* mc = getenv("CQ_TF32_MC");
+  const char* bkv = getenv("CQ_TF32_BK");
   bool wide = n >= 256 && !(bn && atoi(bn) == 128);
   bool multicast = !(mc && atoi(mc) == 1);
+  bool bk16 = bkv && atoi(bkv) == 16;
   int status;
-  if (wide)
-    status = multicast ? tf32::launch<256, 2, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
-                       : tf32::launch<256, 2, 1>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+  if (wide && bk16)
+    status = multicast ? tf32::launch<256, 4, 2, 16>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
+                       : tf32::launch<256, 4, 1, 16>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+  else if (wide)
+    status = multicast ? tf32::launch<256, 2, 2, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
+                       : tf32::launch<256, 2, 1, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
   else
-    status = multicast ? tf32::launch<128, 3, 2>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
-                       : tf32::launch<128, 3, 1>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+    status = multicast ? tf32::launch<128, 3, 2, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
+                       : tf32::launch<128, 3, 1, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
   cudaFreeAsync(scratch, st);
   return status;
 }
