@@ -25,6 +25,9 @@ struct DeviceState {
 DeviceState* device_state(int device);  // nullptr if not initialised
 int ensure_device(int device);           // initialise on first use
 cudaStream_t stream_of(int device, int stream);
+// Grow-only scratch per (device, stream, slot): reused across launches so a
+// captured CUDA graph holds no allocation nodes.  Stream-ordered use only.
+int scratch(int device, int stream, int slot, size_t bytes, void** ptr);
 
 }  // namespace cq
 

@@ -406,11 +406,19 @@ __device__ __forceinline__ void nb_interact2(f32x2 pix, f32x2 piy, f32x2 piz, f3
 
 // NP = i-body pairs per lane (independent FFMA2 chains); a block covers
 // 64*NP i-bodies.
+// The j range [0, n) is cut into NB_JCOLS * NB_WARPS fixed slices: block
+// column y (blockIdx.y) owns NB_WARPS consecutive slices, one per warp.
+// Each block writes its per-body partial (sum over its warps, fixed order)
+// to part_out[y]; nbody_kick_finalize sums the columns in fixed order and
+// applies the kick.  The slicing depends only on n, never on the i range,
+// so a body's acceleration is bit-identical for any GPU count, and the extra
+// grid dimension keeps every SM busy when each GPU owns few i-bodies.
+constexpr int NB_JCOLS = 8;
+
 template <int NP>
 __global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4* __restrict__ pos,
-                                                                   int64_t n, const float4* vel_in,
-                                                                   float4* vel, int64_t i_lo,
-                                                                   int64_t i_hi, float eps2, float dt) {
+                                                                   int64_t n, float* __restrict__ part_out,
+                                                                   int64_t i_lo, int64_t i_hi, float eps2) {
   constexpr int NB_IBLOCK = 64 * NP;
   // j tile, each body duplicated for the packed lanes: (x,x,y,y), (z,z,m,m)
   __shared__ __align__(16) float4 tile[NB_WARPS][32][2];
@@ -429,7 +437,9 @@ __global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4*
     ax[p] = ay[p] = az[p] = 0ull;
   }
   const f32x2 e2 = pack2(eps2, eps2);
-  const int64_t jb = (n * warp) / NB_WARPS, je = (n * (warp + 1)) / NB_WARPS;
+  const int64_t slice = (int64_t)blockIdx.y * NB_WARPS + warp;
+  constexpr int64_t kSlices = (int64_t)NB_JCOLS * NB_WARPS;
+  const int64_t jb = (n * slice) / kSlices, je = (n * (slice + 1)) / kSlices;
   float4 next = (jb + lane < je) ? pos[jb + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t j0 = jb; j0 < je; j0 += 32) {
     tile[warp][lane][0] = make_float4(next.x, next.x, next.y, next.y);
@@ -461,22 +471,43 @@ __global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4*
     part[warp][2][lane + 64 * p + 32] = hi;
   }
   __syncthreads();
-  if (threadIdx.x < NB_IBLOCK) {
-    int64_t i = ibase + threadIdx.x;
+  const int64_t count = i_hi - i_lo;
+  for (int t = threadIdx.x; t < NB_IBLOCK; t += blockDim.x) {
+    int64_t i = ibase + t;
     if (i < i_hi) {
       float sx = 0.f, sy = 0.f, sz = 0.f;
 #pragma unroll
       for (int w = 0; w < NB_WARPS; ++w) {
-        sx += part[w][0][threadIdx.x];
-        sy += part[w][1][threadIdx.x];
-        sz += part[w][2][threadIdx.x];
+        sx += part[w][0][t];
+        sy += part[w][1][t];
+        sz += part[w][2][t];
       }
-      float4 v = vel_in[i - i_lo];
-      v.x = fmaf(dt, sx, v.x);
-      v.y = fmaf(dt, sy, v.y);
-      v.z = fmaf(dt, sz, v.z);
-      vel[i - i_lo] = v;
+      float* o = part_out + ((int64_t)blockIdx.y * count + (i - i_lo)) * 3;
+      o[0] = sx;
+      o[1] = sy;
+      o[2] = sz;
     }
+  }
+}
+
+// v_i += dt * sum over the NB_JCOLS column partials, in column order.
+__global__ void nbody_kick_finalize(const float* __restrict__ part, const float4* vel_in, float4* vel,
+                                    int64_t count, float dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+#pragma unroll
+    for (int c = 0; c < NB_JCOLS; ++c) {
+      const float* p = part + ((int64_t)c * count + i) * 3;
+      sx += p[0];
+      sy += p[1];
+      sz += p[2];
+    }
+    float4 v = vel_in[i];
+    v.x = fmaf(dt, sx, v.x);
+    v.y = fmaf(dt, sy, v.y);
+    v.z = fmaf(dt, sz, v.z);
+    vel[i] = v;
   }
 }
 
@@ -628,46 +659,29 @@ int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const flo
     return e ? atoi(e) : 0;
   }();
   const int64_t bodies = i_hi - i_lo;
-  int use = forced;
-  if (use == 0) {
-    // pick the pairs-per-lane variant with the best expected rate: its
-    // steady-state efficiency (measured on B200 with many waves: NP=4 67.2%,
-    // NP=2 64.5%, NP=1 62.7% of FP32 peak) times the fill of its last wave
-    // (blocks / (SMs x resident blocks per SM), rounded up).  Per-body
-    // results do not depend on NP, so this never changes the bits.
-    static int res[5] = {0, 0, 0, 0, 0};
-    if (!res[1]) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[1], nbody_kick_kernel<1>, NB_WARPS * 32, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[2], nbody_kick_kernel<2>, NB_WARPS * 32, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&res[4], nbody_kick_kernel<4>, NB_WARPS * 32, 0);
-    }
-    const double base[5] = {0, 0.627, 0.645, 0, 0.672};
-    double best = -1.0;
-    for (int p : {4, 2, 1}) {
-      double blocks = (double)((bodies + 64 * p - 1) / (64 * p));
-      double slots = (double)ds->sm_count * (res[p] > 0 ? res[p] : 1);
-      double waves = blocks / slots;
-      double fill = waves / ceil(waves);
-      double eff = base[p] * fill;
-      if (eff > best + 1e-9) {
-        best = eff;
-        use = p;
-      }
-    }
-  }
+  // NB_JCOLS block columns give >= 8x more blocks than i-tiles, so the
+  // widest variant (4 pairs per lane, best steady-state rate) fills the GPU
+  // even at 32768 bodies per GPU; CQ_NBODY_NP overrides for experiments.
+  const int use = forced ? forced : 4;
+  float* part = nullptr;
+  CQ_TRY(scratch(device, stream, 1, (size_t)NB_JCOLS * bodies * 3 * sizeof(float), (void**)&part));
   switch (use) {
-#define NB_LAUNCH(P)                                                                                     \
-  case P:                                                                                              \
-    nbody_kick_kernel<P><<<(unsigned)((bodies + 64 * P - 1) / (64 * P)), NB_WARPS * 32, 0, st>>>(     \
-        (const float4*)pos, n, (const float4*)vel_in, (float4*)vel, i_lo, i_hi, eps2, dt);            \
+#define NB_LAUNCH(P)                                                                                 \
+  case P:                                                                                          \
+    nbody_kick_kernel<P><<<dim3((unsigned)((bodies + 64 * P - 1) / (64 * P)), NB_JCOLS), NB_WARPS * 32, 0, \
+                           st>>>((const float4*)pos, n, part, i_lo, i_hi, eps2);                  \
     break;
     NB_LAUNCH(1)
-    NB_LAUNCH(3)
-    NB_LAUNCH(4)
-    default:
     NB_LAUNCH(2)
+    NB_LAUNCH(3)
+    default:
+    NB_LAUNCH(4)
 #undef NB_LAUNCH
   }
+  CQ_CHECK_LAUNCH();
+  nbody_kick_finalize<<<grid_for(bodies, 256, ds->sm_count, 8), 256, 0, st>>>(
+      part, (const float4*)vel_in, (float4*)vel, bodies, dt);
+  CQ_CHECK_LAUNCH();
   CQ_CHECK_LAUNCH();
   return CQ_OK;
 }

@@ -74,6 +74,26 @@ cudaStream_t stream_of(int device, int stream) {
   return d->streams[stream];
 }
 
+static std::map<std::tuple<int, int, int>, std::pair<void*, size_t>> g_scratch;
+
+int scratch(int device, int stream, int slot, size_t bytes, void** ptr) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto& e = g_scratch[std::make_tuple(device, stream, slot)];
+  if (e.second < bytes) {
+    if (e.first) {
+      // growing: the old block may still be in use by queued work
+      CQ_CHECK_CUDA(cudaStreamSynchronize(stream_of(device, stream)));
+      CQ_CHECK_CUDA(cudaFree(e.first));
+      e.first = nullptr;
+      e.second = 0;
+    }
+    CQ_CHECK_CUDA(cudaMalloc(&e.first, bytes));
+    e.second = bytes;
+  }
+  *ptr = e.first;
+  return CQ_OK;
+}
+
 // ------------------------------------------------------------- memory pool
 // Exact-size free lists per device: repeated runs of the same plan reuse the
 // same blocks without cudaMalloc/cudaFree on the critical path.

@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(SG_THREADS) sgemm_ffma_kernel(const float* __r
   }
 }
 
-int sgemm_3xtf32(cudaStream_t st, int sm_count, const float* a, int64_t lda, const float* b, int64_t ldb,
-                 float* c, int64_t ldc, int64_t m, int64_t n, int64_t k);
+int sgemm_3xtf32(int device, int stream, cudaStream_t st, int sm_count, const float* a, int64_t lda,
+                 const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k);
 
 }  // namespace cq
 
@@ -122,7 +122,7 @@ extern "C" int cq_sgemm(int device, int stream, int variant, const float* a, int
   CQ_CHECK_CUDA(cudaSetDevice(device));
   if (m <= 0 || n <= 0) return CQ_OK;
   if (variant == CQ_SGEMM_3XTF32) {
-    return sgemm_3xtf32(st, device_state(device)->sm_count, a, lda, b, ldb, c, ldc, m, n, k);
+    return sgemm_3xtf32(device, stream, st, device_state(device)->sm_count, a, lda, b, ldb, c, ldc, m, n, k);
   }
   CQ_REQUIRE(variant == CQ_SGEMM_FFMA, "cq_sgemm: unknown variant %d", variant);
   dim3 grid((unsigned)((n + SG_BN - 1) / SG_BN), (unsigned)((m + SG_BM - 1) / SG_BM));

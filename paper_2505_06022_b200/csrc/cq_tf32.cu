@@ -436,15 +436,15 @@ static int launch(cudaStream_t st, const float* ahi, const float* alo, const flo
 
 }  // namespace tf32
 
-int sgemm_3xtf32(cudaStream_t st, int sm_count, const float* a, int64_t lda, const float* b, int64_t ldb,
-                 float* c, int64_t ldc, int64_t m, int64_t n, int64_t k) {
+int sgemm_3xtf32(int device, int stream, cudaStream_t st, int sm_count, const float* a, int64_t lda,
+                 const float* b, int64_t ldb, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k) {
   (void)sm_count;
   CQ_REQUIRE(k % 4 == 0, "3xTF32 sgemm needs k %% 4 == 0 (16-byte TMA row pitch)");
   CQ_REQUIRE(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), "3xTF32 sgemm: dims exceed int32");
-  // scratch for the split operands: 2*(m+n)*k floats, stream-ordered
+  // scratch for the split operands: 2*(m+n)*k floats, reused across calls
   float* scratch = nullptr;
   size_t bytes = (size_t)2 * (size_t)(m + n) * (size_t)k * sizeof(float);
-  CQ_CHECK_CUDA(cudaMallocAsync(&scratch, bytes, st));
+  CQ_TRY(cq::scratch(device, stream, 0, bytes, (void**)&scratch));
   float* ahi = scratch;
   float* alo = ahi + m * k;
   float* bhi = alo + m * k;
@@ -470,7 +470,6 @@ int sgemm_3xtf32(cudaStream_t st, int sm_count, const float* a, int64_t lda, con
   else
     status = multicast ? tf32::launch<128, 3, 2, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
                        : tf32::launch<128, 3, 1, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
-  cudaFreeAsync(scratch, st);
   return status;
 }
 
