@@ -409,10 +409,12 @@ def bench_kernels(args, dist, placement, peaks):
     out = {}
     fp32_peak = lambda mhz: 148 * 128 * 2 * mhz * 1e6 / 1e12  # noqa: E731
 
-    # SAXPY: BASELINE config 0 (2^24, 4 chunks) and a beyond-L2 point 2^28
-    for n, label in ((1 << 24, "saxpy_2p24"), (1 << 28, "saxpy_2p28")):
+    # SAXPY: BASELINE config 0 exactly (2^24, one_to_one split into 4 chunks:
+    # 4 plan nodes placed on the available GPUs) and a beyond-L2 point 2^28
+    for n, label, nodes in ((1 << 24, "saxpy_2p24_4chunks", max(4, world)),
+                            (1 << 28, "saxpy_2p28", world)):
         prog = W.saxpy_program(n, kind="float32")
-        plan = cq.generate_commands(prog.graph(), world)
+        plan = cq.generate_commands(prog.graph(), nodes)
         sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=20)
         k = kinds.get("saxpy", [0, 1.0, 1])
         achieved = dist.min(12 * k[0] / (k[1] / 1e3) / 1e9)

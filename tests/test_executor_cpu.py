@@ -114,6 +114,16 @@ def _free_port():
     return port
 
 
+def _nbody_prog():
+    pos, vel = W.nbody_inputs(96)
+    return W.nbody_program(96, steps=2, pos=pos, vel=vel)
+
+
+def _sgemm_prog():
+    a, b = W.sgemm_inputs(40, 24, 16)
+    return W.sgemm_program(40, 24, 16, a=a, b=b)
+
+
 def _rank_main(rank, world, port, outdir):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -140,6 +150,15 @@ def _rank_main(rank, world, port, outdir):
         if rank == 0:
             for name in buffers:
                 results[f"g{idx}__{name}"] = res.buffers[name]
+    # N-body: the 'all' mapper's pushes = an all-gather group per step;
+    # sgemm: A slabs scattered, B broadcast (host-init lowering at each rank)
+    for nodes in (2, 3):
+        res = E.run(cq.generate_commands(_nbody_prog().graph(), nodes), placement=pl)
+        if rank == 0:
+            results[f"nbody{nodes}_P"], results[f"nbody{nodes}_V"] = res.buffers["P"], res.buffers["V"]
+        res = E.run(cq.generate_commands(_sgemm_prog().graph(), nodes), placement=pl)
+        if rank == 0:
+            results[f"sgemm{nodes}_C"] = res.buffers["C"]
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), **results)
     dist.barrier()
     dist.destroy_process_group()
@@ -164,6 +183,15 @@ def test_two_ranks_gloo(tmp_path):
         if key.startswith("g"):
             idx, name = key[1:].split("__")
             assert dsl.same_bits(val, EXPECTED[f"p{idx}__{name}"]), key
+    # the distributed runs equal a single-process run of the same double
+    N._lib = FakeLib(1, LocalTransport())
+    single_nb = E.run(cq.generate_commands(_nbody_prog().graph(), 1), placement=E.Placement(1, 0, (0,)))
+    single_mm = E.run(cq.generate_commands(_sgemm_prog().graph(), 1), placement=E.Placement(1, 0, (0,)))
+    N._lib = None
+    for nodes in (2, 3):
+        assert dsl.same_bits(r0[f"nbody{nodes}_P"], single_nb.buffers["P"])
+        assert dsl.same_bits(r0[f"nbody{nodes}_V"], single_nb.buffers["V"])
+        assert dsl.same_bits(r0[f"sgemm{nodes}_C"], single_mm.buffers["C"])
 
 
 def test_graph_capture_replays_same_commands(fake):
