@@ -217,6 +217,14 @@ def bench_wave(args, dist, placement, peaks):
     kern_ms = sum(sess.elapsed_ms(a, b) for _k, _c, _d, _s, a, b in dominant)
     kern_bytes = sum(12 * cells for _k, cells, *_ in dominant)
     sess.recycle()
+    timing_source = "stream-traced replay"
+    if not args.no_graph:
+        def select(log):
+            return [x for x in log if x[0] == "wave5" and x[1] == dom_launch[1]]
+        g = graph_launch_times(sess, 2, select)
+        if g and "wave5" in g:
+            kern_bytes, kern_ms = 12 * g["wave5"][0], g["wave5"][1]
+            timing_source = "timed CUDA-graph replay (event-record nodes)"
     # the timed replays run as one CUDA graph per rank (kernels, copies and
     # NCCL groups captured once), so no per-command host dispatch remains
     replay_mode = "cuda_graph"
@@ -302,7 +310,8 @@ def bench_wave(args, dist, placement, peaks):
                      "kernel": "wave5_rows_kernel<float,32>", "bytes_per_cell": 12,
                      "cells_per_launch": dom_launch[1], "launches": len(dominant),
                      "bytes_per_launch": 12 * dom_launch[1],
-                     "peak_source": peaks[1] + " hbm_gbs (torch copy)"},
+                     "peak_source": peaks[1] + " hbm_gbs (torch copy)",
+                     "launch_timing": timing_source},
         "clocks": clk,
         "gpu_launches": gpu_launches,
         "replay": replay_mode,
@@ -312,6 +321,35 @@ def bench_wave(args, dist, placement, peaks):
 
 
 # -------------------------------------------------------- other BASELINE kernels
+
+def graph_launch_times(sess, reps, select=None):
+    """Per-launch CUDA-event durations of the dominant kernels, read from
+    ``reps`` replays of a timed CUDA graph (event-record nodes around every
+    launch): the launches run exactly as in the timed region, back to back
+    with no host dispatch between them.  Returns {kind: [cells, ms, launches]}
+    over the launches ``select(log)`` keeps (default: all), or None when the
+    graph cannot be captured (then the caller keeps its stream-traced times)."""
+    try:
+        sess.capture(timed=True)
+    except Exception:  # noqa: BLE001
+        sess.synchronize()
+        sess.recycle()
+        return None
+    sess.replay(1)
+    sess.synchronize()
+    per_kind = {}
+    for _ in range(reps):
+        sess.replay(1)
+        sess.synchronize()
+        log = sess.graph_log if select is None else select(sess.graph_log)
+        for kind, cells, _d, _s, a, b in log:
+            k = per_kind.setdefault(kind, [0, 0.0, 0])
+            k[0] += cells
+            k[1] += sess.elapsed_ms(a, b)
+            k[2] += 1
+    sess.recycle()
+    return per_kind
+
 
 def _timed_session(plan, placement, dist, reps, warm=2):
     from paper_2505_06022_b200 import executor as E
@@ -323,7 +361,7 @@ def _timed_session(plan, placement, dist, reps, warm=2):
         sess.execute(upload=False)
         sess.synchronize()
         sess.recycle()
-    # traced replay: per-kernel CUDA-event times
+    # traced stream replay (fallback only: host dispatch gaps inflate short launches)
     sess.execute(upload=False)
     sess.synchronize()
     log = [(k, c * reps, d, s, a, b) for k, c, d, s, a, b in sess.launch_log]
@@ -334,6 +372,7 @@ def _timed_session(plan, placement, dist, reps, warm=2):
         k[1] += sess.elapsed_ms(a, b) * reps
         k[2] += reps
     sess.recycle()
+    per_kind = graph_launch_times(sess, reps) or per_kind
     graph = True
     try:
         sess.capture()
@@ -421,7 +460,9 @@ def bench_kernels(args, dist, placement, peaks):
         out[label] = {"value": 12 * n * 20 / (ms / 1e3) / 1e9, "unit": "GB/s", "scaling": "strong",
                       "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],
                                    "frac": achieved / peaks[0]["hbm_gbs"]},
-                      "note": "2^24 x fp32 (192 MiB) fits in L2" if n == 1 << 24 else "inputs > L2"}
+                      "chunks": nodes, "launch_timing": "timed CUDA-graph replay",
+                      "note": ("BASELINE config 0: 2^24 x fp32, 192 MiB per pass (> 126 MB L2; "
+                               "back-to-back passes partly hit L2)") if n == 1 << 24 else "inputs > L2"}
         sess.close()
 
     # wave variants: float64 (the reference's own element kind, 24 B/cell/step,

@@ -103,6 +103,11 @@ int cq_unpack_box(int device, int stream, int elem_bytes, const cq_view_t* dst,
 int cq_event_create(int device, int timing, uint64_t* event);
 int cq_event_destroy(uint64_t event);
 int cq_event_record(uint64_t event, int device, int stream);
+/* A timestamp that survives graph capture: while `stream` is being captured
+ * it becomes an event-record node (re-recorded on every replay, so the
+ * per-launch times of the replayed graph can be read back); otherwise it is
+ * cq_event_record.  Trace-only: never waited on. */
+int cq_event_record_timed(uint64_t event, int device, int stream);
 int cq_stream_wait_event(int device, int stream, uint64_t event);
 int cq_event_synchronize(uint64_t event);
 int cq_event_elapsed_ms(uint64_t start, uint64_t stop, float* ms);

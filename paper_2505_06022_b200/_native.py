@@ -76,6 +76,7 @@ _SIGS = {
     "cq_event_create": (i32, [i32, i32, P(u64)]),
     "cq_event_destroy": (i32, [u64]),
     "cq_event_record": (i32, [u64, i32, i32]),
+    "cq_event_record_timed": (i32, [u64, i32, i32]),
     "cq_stream_wait_event": (i32, [i32, i32, u64]),
     "cq_event_synchronize": (i32, [u64]),
     "cq_event_elapsed_ms": (i32, [u64, u64, P(ctypes.c_float)]),

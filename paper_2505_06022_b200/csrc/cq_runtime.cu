@@ -433,6 +433,17 @@ int cq_event_record(uint64_t event, int device, int stream) {
   return CQ_OK;
 }
 
+int cq_event_record_timed(uint64_t event, int device, int stream) {
+  CQ_STREAM(device, stream);
+  cudaStreamCaptureStatus cs;
+  CQ_CHECK_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    CQ_CHECK_CUDA(cudaEventRecordWithFlags((cudaEvent_t)(uintptr_t)event, st, cudaEventRecordExternal));
+  else
+    CQ_CHECK_CUDA(cudaEventRecord((cudaEvent_t)(uintptr_t)event, st));
+  return CQ_OK;
+}
+
 int cq_stream_wait_event(int device, int stream, uint64_t event) {
   CQ_STREAM(device, stream);
   CQ_CHECK_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)(uintptr_t)event, 0));

@@ -407,6 +407,10 @@ class Session:
         self.bindings = {}
         self.trace_marks = []   # per command: timing events for the trace
         self.launch_log = []    # (binding kind, cells, device, start, stop) per kernel launch
+        self.capturing = False
+        self.graph = None
+        self.graph_log = []     # launch_log of a timed capture: its events re-record per replay
+        self.graph_events = []
         self.host_init = {}
         self._sched = None
         self.t0 = None
@@ -460,15 +464,20 @@ class Session:
         skey = (device, stream)
         for ev, _sk in self.haz.waits(accesses, skey).items():
             N.call("cq_stream_wait_event", device, stream, ctypes.c_uint64(ev))
-        start = None
+        start = tstop = None
         if self.want_trace:
             start = self.event(device, timing=True)
-            N.call("cq_event_record", ctypes.c_uint64(start), device, stream)
+            N.call("cq_event_record_timed", ctypes.c_uint64(start), device, stream)
         fn()
-        stop = self.event(device, timing=self.want_trace)
+        if self.want_trace and self.capturing:
+            # inside a capture the hazard event only becomes a graph edge;
+            # the timestamp needs its own event-record node
+            tstop = self.event(device, timing=True)
+            N.call("cq_event_record_timed", ctypes.c_uint64(tstop), device, stream)
+        stop = self.event(device, timing=self.want_trace and not self.capturing)
         N.call("cq_event_record", ctypes.c_uint64(stop), device, stream)
         self.haz.record(accesses, skey, stop)
-        return start, stop
+        return start, tstop or stop
 
     # ---- allocation ----------------------------------------------------
     def allocate(self):
@@ -974,19 +983,24 @@ class Session:
             elif self.local(step[1].node):
                 self.exec_command(step[1], step[2])
 
-    def capture(self):
+    def capture(self, timed: bool = False):
         """Capture one replay of the plan (``execute(upload=False)``) into a
         CUDA graph -- kernels, copies, NCCL groups and the cross-stream event
         edges -- so later replays cost one launch instead of one Python
         dispatch per command.  One local device only (the one-rank-per-GPU
-        layout)."""
+        layout).
+
+        timed=True brackets every launch with event-record nodes; after each
+        replay (and a synchronize) ``graph_log`` holds that replay's per-launch
+        (kind, cells, device, stream, start, stop) events."""
         if len(self.devices) != 1:
             raise ValidationError("graph capture needs exactly one local device")
         d = self.devices[0]
         self.synchronize()
         self.recycle()
         saved = self.want_trace
-        self.want_trace = False
+        self.want_trace = timed
+        self.capturing = True
         N.call("cq_graph_begin", d)
         handle = ctypes.c_uint64()
         try:
@@ -997,15 +1011,35 @@ class Session:
                 N.call("cq_graph_destroy", handle)
             except NativeError:
                 pass
-            self.want_trace = saved
+            self.want_trace, self.capturing = saved, False
+            self.recycle()
             raise
+        finally:
+            self.capturing = False
         N.call("cq_graph_end", d, ctypes.byref(handle))
         self.want_trace = saved
-        self.recycle()  # events recorded during capture are graph-internal
-        if getattr(self, "graph", None):
-            N.call("cq_graph_destroy", ctypes.c_uint64(self.graph))
+        self._drop_graph()
+        log = list(self.launch_log)
+        if timed:
+            # the graph's event-record nodes own these events: keep them out
+            # of the recycling pool for the graph's lifetime
+            self.graph_events = [ev for _d, _t, ev in self.events]
+            self.events = []
+        self.recycle()  # other events recorded during capture are graph-internal
         self.graph = handle.value
+        self.graph_log = log if timed else []
         return self.graph
+
+    def _drop_graph(self):
+        if self.graph:
+            for d in self.devices:
+                N.call("cq_stream_synchronize", d, N.STREAM_COMPUTE)
+            N.call("cq_graph_destroy", ctypes.c_uint64(self.graph))
+            self.graph = None
+        for ev in self.graph_events:
+            N.call("cq_event_destroy", ctypes.c_uint64(ev))
+        self.graph_events = []
+        self.graph_log = []
 
     def replay(self, times: int = 1):
         """Launch the captured graph ``times`` times (asynchronous)."""
@@ -1061,11 +1095,7 @@ class Session:
         self._t0 = {}
 
     def close(self):
-        if getattr(self, "graph", None):
-            for d in self.devices:
-                N.call("cq_stream_synchronize", d, N.STREAM_COMPUTE)
-            N.call("cq_graph_destroy", ctypes.c_uint64(self.graph))
-            self.graph = None
+        self._drop_graph()
         self.release()
         for pool in self.free_events.values():
             for ev in pool:

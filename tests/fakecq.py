@@ -171,6 +171,9 @@ class FakeLib:
     def cq_event_record(self, e, d, s):
         return 0
 
+    def cq_event_record_timed(self, e, d, s):
+        return 0
+
     def cq_stream_wait_event(self, d, s, e):
         return 0
 

@@ -209,4 +209,14 @@ def test_graph_capture_replays_same_commands(fake):
     s.replay(2)
     s.synchronize()
     assert lib.launches.count("wave5") == 3 * base
+    assert s.graph_log == [] and s.graph_events == []
+    # timed capture: the launch log survives, its events stay out of the pool
+    s.capture(timed=True)
+    assert len([x for x in s.graph_log if x[0] == "wave5"]) == base
+    held = set(s.graph_events)
+    assert held and not held & {ev for pool in s.free_events.values() for ev in pool}
+    s.replay(1)
+    s.synchronize()
+    assert lib.launches.count("wave5") == 4 * base
     s.close()
+    assert s.graph is None and s.graph_events == []

@@ -244,18 +244,25 @@ def test_graph_replay_equals_plain_replay(nodes):
     prog = W.wave_program(h, w, steps=6, kind="float32", u0=u0, up0=u0)
     plan = cq.generate_commands(prog.graph(), nodes)
     out = []
-    for graph in (False, True):
+    for graph in (False, True, "timed"):
         s = Session(plan, Placement(1, 0, (0,)))
         s.execute(upload=True)
         s.synchronize()
         s.recycle()
         if graph:
-            s.capture()
+            s.capture(timed=graph == "timed")
             s.replay(3)
         else:
             for _ in range(3):
                 s.execute(upload=False)
         s.synchronize()
+        if graph == "timed":
+            # one (start, stop) pair of event-record nodes per launch, re-taken per replay
+            waves = [x for x in s.graph_log if x[0] == "wave5"]
+            assert len(waves) >= 6
+            times = [s.elapsed_ms(a, b) for _k, _c, _d, _s, a, b in waves]
+            assert all(0.0 < t < 1e3 for t in times)
         out.append(s.results())
         s.close()
-    assert dsl.same_bits(out[0]["u"], out[1]["u"]) and dsl.same_bits(out[0]["up"], out[1]["up"])
+    for o in out[1:]:
+        assert dsl.same_bits(out[0]["u"], o["u"]) and dsl.same_bits(out[0]["up"], o["up"])
