@@ -332,6 +332,215 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------ 2-SM variant
+// A CTA pair (cluster of 2) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (M = 256): CTA r keeps A rows [128r, 128r+128)
+// and B rows (n) [r*BN/2, (r+1)*BN/2) of the tile in its own shared memory
+// (same offsets in both CTAs), the leader (r = 0) issues every MMA, and each
+// CTA's TMEM receives its own 128 rows x BN columns.  Against the 1-SM kernel
+// this halves the B bytes each SM stages and feeds to the tensor core per
+// MMA, so per-SM shared-memory traffic drops from 5 to 3.3 KB per 8-wide k
+// step of one product -- less energy per flop under the power cap.
+// Tiles are rasterised in groups of `group_m` pairs down M, so a wave of
+// clusters reads a compact block of A rows and B columns (L2 reuse) rather
+// than all of B.
+template <int BN, int STAGES, int BK>
+struct Smem2 {
+  float a_hi[STAGES][BM * BK];
+  float a_lo[STAGES][BM * BK];
+  float b_hi[STAGES][BN / 2 * BK];
+  float b_lo[STAGES][BN / 2 * BK];
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+// TMA load of this CTA's half; completion bytes go to the leader's barrier
+// (the peer bit of the shared::cluster address cleared).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// completion of the pair's MMAs -> arrive on the barrier at this offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, 0;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int BN, int STAGES, int BK>
+__global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
+    sgemm_3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
+                            const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                            float* __restrict__ C, int64_t ldc, int m, int n, int k, int group_kb, int pairs_m,
+                            int tiles_n, int group_m) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem2<BN, STAGES, BK>& S = *reinterpret_cast<Smem2<BN, STAGES, BK>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_rank();
+  // grouped rasterisation of (m pair, n tile) over the linear cluster index
+  const int pair = blockIdx.x >> 1;
+  const int per_group = group_m * tiles_n;
+  const int first = (pair / per_group) * group_m;
+  const int gsize = min(pairs_m - first, group_m);
+  const int pm = first + (pair % per_group) % gsize;
+  const int tn = (pair % per_group) / gsize;
+  const int row0 = (pm * 2 + (int)crank) * BM;
+  const int col0 = tn * BN;
+  const int num_kb = (k + BK - 1) / BK;
+  const int num_groups = (num_kb + group_kb - 1) / group_kb;
+  constexpr uint32_t kStageBytes = (2 * BM * BK + 2 * (BN / 2) * BK) * sizeof(float);
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_ahi);
+    prefetch_map(&map_alo);
+    prefetch_map(&map_bhi);
+    prefetch_map(&map_blo);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&S.full[s], 1);   // the leader's expect_tx arrival; both CTAs' bytes
+      mbar_init(&S.empty[s], 1);  // the leader's multicast MMA commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.tfull[b], 1);
+      mbar_init(&S.tempty[b], 2 * Epi<BN>::kWarps);  // both CTAs' epilogue warps (leader's copy)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                 "r"(Epi<BN>::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t phase = (kb / STAGES) & 1;
+        mbar_wait(&S.empty[s], phase ^ 1);
+        if (crank == 0) mbar_expect_tx(&S.full[s], 2 * kStageBytes);
+        const uint32_t bar = smem_u32(&S.full[s]) & 0xFEFFFFFFu;
+        const int kc = kb * BK;
+        tma_load_2d_pair(S.a_hi[s], &map_ahi, bar, kc, row0);
+        tma_load_2d_pair(S.a_lo[s], &map_alo, bar, kc, row0);
+        tma_load_2d_pair(S.b_hi[s], &map_bhi, bar, kc, col0 + (int)crank * (BN / 2));
+        tma_load_2d_pair(S.b_lo[s], &map_blo, bar, kc, col0 + (int)crank * (BN / 2));
+      }
+      // every multicast commit on this CTA's stage barriers has landed
+      for (int kb = num_kb; kb < num_kb + STAGES; ++kb) mbar_wait(&S.empty[kb % STAGES], ((kb / STAGES) & 1) ^ 1);
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && crank == 0) {
+      constexpr uint32_t idesc = instr_desc(2 * BM, BN);
+      int kb = 0;
+      for (int g = 0; g < num_groups; ++g) {
+        const int buf = g & 1;
+        mbar_wait(&S.tempty[buf], ((g >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc_addr = tmem + (uint32_t)(buf * BN);
+        const int kb_end = min(kb + group_kb, num_kb);
+        for (int first_kb = kb; kb < kb_end; ++kb) {
+          const int s = kb % STAGES;
+          mbar_wait(&S.full[s], (kb / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint64_t dah = smem_desc<BK>(S.a_hi[s]), dal = smem_desc<BK>(S.a_lo[s]);
+          const uint64_t dbh = smem_desc<BK>(S.b_hi[s]), dbl = smem_desc<BK>(S.b_lo[s]);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t o = (uint64_t)(kk * 2);
+            mma_tf32_pair(acc_addr, dah + o, dbh + o, idesc, (kb != first_kb || kk != 0) ? 1u : 0u);
+            mma_tf32_pair(acc_addr, dah + o, dbl + o, idesc, 1);
+            mma_tf32_pair(acc_addr, dal + o, dbh + o, idesc, 1);
+          }
+          mma_commit_pair(&S.empty[s]);
+        }
+        mma_commit_pair(&S.tfull[buf]);
+      }
+    }
+  } else {
+    const int e = warp - 2;
+    const int lane_group = warp & 3;
+    const int seg = e >> 2;
+    float acc[64];
+#pragma unroll
+    for (int q = 0; q < 64; ++q) acc[q] = 0.f;
+    for (int g = 0; g < num_groups; ++g) {
+      const int buf = g & 1;
+      mbar_wait(&S.tfull[buf], (g >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t base = tmem + ((uint32_t)(lane_group * 32) << 16) + (uint32_t)(buf * BN + seg * 64);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t r[16];
+        tmem_ld16(base + (uint32_t)(h * 16), r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[h * 16 + q] += __uint_as_float(r[q]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&S.tempty[buf]);
+    }
+    const int row = row0 + lane_group * 32 + lane;
+    const int col = col0 + seg * 64;
+    if (row < m && col < n) {
+      float* dst = C + (int64_t)row * ldc + col;
+      if (col + 64 <= n && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          reinterpret_cast<float4*>(dst)[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 64; ++q)
+          if (col + q < n) dst[q] = acc[q];
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Epi<BN>::kTmemCols));
+  }
+}
+
 // ---------------------------------------------------------------- split pass
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
@@ -434,6 +643,40 @@ static int launch(cudaStream_t st, const float* ahi, const float* alo, const flo
   return CQ_OK;
 }
 
+template <int BN, int STAGES, int BK>
+static int launch_2sm(cudaStream_t st, const float* ahi, const float* alo, const float* bhi, const float* blo,
+                      float* c, int64_t ldc, int64_t m, int64_t n, int64_t k) {
+  CUtensorMap ma, mal, mb, mbl;
+  CQ_TRY(make_map(&ma, ahi, m, k, BM, BK));
+  CQ_TRY(make_map(&mal, alo, m, k, BM, BK));
+  CQ_TRY(make_map(&mb, bhi, n, k, BN / 2, BK));
+  CQ_TRY(make_map(&mbl, blo, n, k, BN / 2, BK));
+  size_t smem = sizeof(Smem2<BN, STAGES, BK>) + 1024;
+  auto kern = sgemm_3xtf32_2sm_kernel<BN, STAGES, BK>;
+  CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int pairs_m = (int)((m + 2 * BM - 1) / (2 * BM));
+  const int tiles_n = (int)((n + BN - 1) / BN);
+  int group_kb = 128 / BK;
+  if (const char* g = getenv("CQ_TF32_GROUP_KB")) group_kb = atoi(g) > 0 ? atoi(g) : group_kb;
+  int group_m = 8;
+  if (const char* g = getenv("CQ_TF32_GROUP_M")) group_m = atoi(g) > 0 ? atoi(g) : group_m;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs_m * tiles_n));
+  cfg.blockDim = dim3(Epi<BN>::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CQ_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mal, mb, mbl, c, ldc, (int)m, (int)n, (int)k, group_kb, pairs_m,
+                                   tiles_n, group_m));
+  return CQ_OK;
+}
+
 }  // namespace tf32
 
 int sgemm_3xtf32(int device, int stream, cudaStream_t st, int sm_count, const float* a, int64_t lda,
@@ -460,8 +703,12 @@ int sgemm_3xtf32(int device, int stream, cudaStream_t st, int sm_count, const fl
   bool wide = n >= 256 && !(bn && atoi(bn) == 128);
   bool multicast = !(mc && atoi(mc) == 1);
   bool bk16 = bkv && atoi(bkv) == 16;
+  const char* pair = getenv("CQ_TF32_2SM");
+  bool two_sm = wide && !(pair && atoi(pair) == 0);
   int status;
-  if (wide && bk16)
+  if (two_sm)
+    status = tf32::launch_2sm<256, 3, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+  else if (wide && bk16)
     status = multicast ? tf32::launch<256, 4, 2, 16>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
                        : tf32::launch<256, 4, 1, 16>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
   else if (wide)
