@@ -682,7 +682,6 @@ int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const flo
   nbody_kick_finalize<<<grid_for(bodies, 256, ds->sm_count, 8), 256, 0, st>>>(
       part, (const float4*)vel_in, (float4*)vel, bodies, dt);
   CQ_CHECK_LAUNCH();
-  CQ_CHECK_LAUNCH();
   return CQ_OK;
 }
 
