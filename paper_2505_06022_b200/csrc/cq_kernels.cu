@@ -372,6 +372,11 @@ __device__ __forceinline__ f32x2 pack2(float lo, float hi) {
 __device__ __forceinline__ void unpack2(f32x2 v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
   f32x2 r;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -523,6 +528,106 @@ __global__ void nbody_drift_kernel(const float4* p_in, const float4* __restrict_
   }
 }
 
+// ---------------------------------------------- wave 5pt, KL steps per pass
+// Temporal blocking of the wave ping-pong: from X(t) (u) and X(t-1) (upr)
+// one pass computes X(t+1) .. X(t+KL) on chip and writes only X(t+KL)
+// (out_last) and X(t+KL-1) (out_prev): 16 B/cell per KL steps instead of
+// 12 B/cell per step.  Every intermediate cell is the same DSL tree with the
+// same operands as the one-step kernel (wave_cell order, one rounding per
+// operator, packed FP32x2 lanes are per-lane IEEE RN), so the result is
+// bit-identical to KL launches of wave5_rows_kernel.
+//
+// A warp owns a strip of 128 loaded columns (lane = 4 columns) and emits the
+// middle 128 - 2*KL: level j is exact on columns [j, 128-j) of the strip
+// (west/east neighbours by shuffle; the strip edge loses one column per
+// level).  It marches RB output rows, loading rows [r0-KL, r1+KL) of the
+// inputs, keeping a 3-row window per level in registers (slot = row mod 3,
+// unrolled so every slot index is static) and prefetching input rows 3
+// ahead.  Global borders clamp exactly like the DSL's ReadView (the border
+// cell reads itself).  Rows outside [in_lo, in_hi) are not read; the caller
+// keeps [out_lo, out_hi) inside the trapezoid they determine.
+__device__ __forceinline__ float4 wave4_packed(float4 m, float4 n, float4 s, float4 p, float wv, float ev,
+                                               f32x2 c2, f32x2 k22, f32x2 k42) {
+  const f32x2 uA = pack2(m.x, m.y), uB = pack2(m.z, m.w);
+  const f32x2 mid = pack2(m.y, m.z);  // east of A == west of B
+  const f32x2 lapA = sub2(add2(add2(add2(pack2(n.x, n.y), pack2(s.x, s.y)), pack2(wv, m.x)), mid), mul2(k42, uA));
+  const f32x2 lapB = sub2(add2(add2(add2(pack2(n.z, n.w), pack2(s.z, s.w)), mid), pack2(m.w, ev)), mul2(k42, uB));
+  const f32x2 oA = add2(sub2(mul2(k22, uA), pack2(p.x, p.y)), mul2(c2, lapA));
+  const f32x2 oB = add2(sub2(mul2(k22, uB), pack2(p.z, p.w)), mul2(c2, lapB));
+  float4 o;
+  unpack2(oA, o.x, o.y);
+  unpack2(oB, o.z, o.w);
+  return o;
+}
+
+template <int KL, int RB>
+__global__ void __launch_bounds__(256) wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last,
+                                                          cq_view_t out_prev, int64_t in_lo, int64_t in_hi,
+                                                          int64_t out_lo, int64_t out_hi, int64_t H, int64_t W,
+                                                          float c, float k2, float k4) {
+  static_assert(KL >= 2 && KL % 4 == 0, "strip offsets must stay 16-byte aligned");
+  constexpr int SW = 128 - 2 * KL;
+  const int lane = threadIdx.x & 31;
+  const int64_t strip = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t r0 = out_lo + (int64_t)blockIdx.y * RB;
+  if (strip * SW >= W || r0 >= out_hi) return;  // warp-uniform
+  const int64_t r1 = min(r0 + (int64_t)RB, out_hi);
+  const int64_t col = strip * SW - KL + lane * 4;
+  const bool colok = col >= 0 && col < W;
+  const bool keep = lane >= KL / 4 && lane < 32 - KL / 4 && col < W;
+  const bool at_w = col == 0, at_e = col + 4 == W;
+  const f32x2 c2 = pack2(c, c), k22 = pack2(k2, k2), k42 = pack2(k4, k4);
+  auto ld = [&](const cq_view_t& v, int64_t r) -> float4 {
+    if (!colok || r < in_lo || r >= in_hi) return make_float4(0.f, 0.f, 0.f, 0.f);
+    return __ldcs(reinterpret_cast<const float4*>((const float*)v.ptr + (r - v.alloc.lo[1]) * v.stride[1] +
+                                                  (col - v.alloc.lo[2])));
+  };
+  auto st = [&](const cq_view_t& v, int64_t r, float4 x) {
+    if (keep && r >= r0 && r < r1)
+      __stcs(reinterpret_cast<float4*>((float*)v.ptr + (r - v.alloc.lo[1]) * v.stride[1] + (col - v.alloc.lo[2])),
+             x);
+  };
+  float4 L[KL][3];  // level j (0 = X(t)) rows, slot = (row - rb) % 3
+  float4 P[3];      // X(t-1) rows
+  float4 Q[3], QP[3];
+  const int64_t rb = r0 - KL, re = r1 + KL;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    Q[q] = ld(u, rb + q);
+    QP[q] = ld(upr, rb + q);
+  }
+#pragma unroll 1
+  for (int64_t base = rb; base < re; base += 3) {
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      const int64_t ri = base + s;
+      if (ri < re) {
+        L[0][s] = Q[s];
+        P[s] = QP[s];
+        Q[s] = ld(u, ri + 3);
+        QP[s] = ld(upr, ri + 3);
+        const int so = (s + 1) % 3, sm = (s + 2) % 3;  // slots of rows ri-2, ri-1
+#pragma unroll
+        for (int j = 1; j <= KL; ++j) {
+          const int64_t rho = ri - j;
+          const float4 mid = L[j - 1][sm];
+          const float4 nn = (rho == 0) ? mid : L[j - 1][so];
+          const float4 ss = (rho == H - 1) ? mid : L[j - 1][s];
+          const float4 pp = (j == 1) ? P[sm] : L[j >= 2 ? j - 2 : 0][so];
+          float wv = __shfl_up_sync(0xffffffffu, mid.w, 1);
+          float ev = __shfl_down_sync(0xffffffffu, mid.x, 1);
+          if (at_w) wv = mid.x;
+          if (at_e) ev = mid.w;
+          const float4 o = wave4_packed(mid, nn, ss, pp, wv, ev, c2, k22, k42);
+          if (j < KL) L[j][s] = o;
+          if (j == KL - 1) st(out_prev, rho, o);
+          if (j == KL) st(out_last, rho, o);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace cq
 
 using namespace cq;
@@ -612,6 +717,41 @@ int cq_wave5(int device, int stream, int kind, const cq_view_t* u, const cq_view
     else
       wave5_cell_kernel<double><<<grid, 256, 0, st>>>(*u, *upr, *out, *box, H, W, c, k2, k4);
   }
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_wave5_fused(int device, int stream, int levels, const cq_view_t* u, const cq_view_t* upr,
+                   const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
+                   int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4) {
+  CQ_GET_STREAM(device, stream);
+  if (out_hi <= out_lo) return CQ_OK;
+  const int64_t H = extent->hi[1], W = extent->hi[2];
+  CQ_REQUIRE(levels == 4 || levels == 8, "cq_wave5_fused: levels must be 4 or 8 (got %d)", levels);
+  CQ_REQUIRE(W % 4 == 0, "cq_wave5_fused: row length must be a multiple of 4");
+  for (const cq_view_t* v : {u, upr, out_last, out_prev}) {
+    CQ_REQUIRE(((uintptr_t)v->ptr % 16 == 0) && v->stride[1] % 4 == 0 && v->alloc.lo[2] == 0 &&
+                   v->alloc.hi[2] == W && v->stride[2] == 1,
+               "cq_wave5_fused: views must hold whole 16-byte aligned rows");
+  }
+  CQ_REQUIRE(out_last->ptr != u->ptr && out_last->ptr != upr->ptr && out_prev->ptr != u->ptr &&
+                 out_prev->ptr != upr->ptr && out_last->ptr != out_prev->ptr,
+             "cq_wave5_fused: outputs must not alias the inputs");
+  // the trapezoid: level L is exact on rows [in_lo + L, in_hi - L), except at the true borders
+  const int64_t lo_ok = in_lo == 0 ? 0 : in_lo + levels, hi_ok = in_hi == H ? H : in_hi - levels;
+  CQ_REQUIRE(out_lo >= lo_ok && out_hi <= hi_ok && in_lo >= 0 && in_hi <= H,
+             "cq_wave5_fused: rows [%lld, %lld) are not determined by input rows [%lld, %lld)",
+             (long long)out_lo, (long long)out_hi, (long long)in_lo, (long long)in_hi);
+  constexpr int RB = 128;
+  const int sw = 128 - 2 * levels;
+  const int64_t strips = (W + sw - 1) / sw;
+  dim3 grid((unsigned)((strips + 7) / 8), (unsigned)((out_hi - out_lo + RB - 1) / RB));
+  if (levels == 4)
+    wave5_fused_kernel<4, RB><<<grid, 256, 0, st>>>(*u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H,
+                                                    W, (float)c, (float)k2, (float)k4);
+  else
+    wave5_fused_kernel<8, RB><<<grid, 256, 0, st>>>(*u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H,
+                                                    W, (float)c, (float)k2, (float)k4);
   CQ_CHECK_LAUNCH();
   return CQ_OK;
 }

@@ -1,0 +1,110 @@
+"""GPU check of cq_wave5_fused (KL steps per pass) against KL launches of
+cq_wave5: bit-identical on full grids and on row slabs, then timing at 16384^2."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402  (device memory only)
+
+from paper_2505_06022_b200 import _native as N  # noqa: E402
+
+N.call("cq_init_device", 0)
+C, K2, K4 = 0.25, 2.0, 4.0
+
+
+def view(t, h, w):
+    v = N.CqView()
+    v.ptr = t.data_ptr()
+    v.alloc = N.box3((0, 0), (h, w))
+    v.stride[:] = [h * w, w, 1]
+    return v
+
+
+def plain(a, b, h, w, steps, rows=None):
+    """steps one-step launches, ping-pong in place; returns (X(t+steps), X(t+steps-1))."""
+    a, b = a.clone(), b.clone()
+    ext = N.box3((0, 0), (h, w))
+    box = N.box3((0, 0), (h, w)) if rows is None else N.box3((rows[0], 0), (rows[1], w))
+    for _ in range(steps):
+        N.call("cq_wave5", 0, 0, N.CQ_F32, ctypes.byref(view(a, h, w)), ctypes.byref(view(b, h, w)),
+               ctypes.byref(view(b, h, w)), ctypes.byref(box), ctypes.byref(ext), C, K2, K4)
+        a, b = b, a
+    return a, b
+
+
+def fused(a, b, h, w, kl, in_rows, out_rows):
+    ol, op = torch.full_like(a, float("nan")), torch.full_like(a, float("nan"))
+    ext = N.box3((0, 0), (h, w))
+    N.call("cq_wave5_fused", 0, 0, kl, ctypes.byref(view(a, h, w)), ctypes.byref(view(b, h, w)),
+           ctypes.byref(view(ol, h, w)), ctypes.byref(view(op, h, w)), in_rows[0], in_rows[1],
+           out_rows[0], out_rows[1], ctypes.byref(ext), C, K2, K4)
+    return ol, op
+
+
+def same(x, y):
+    return torch.equal(x.view(torch.int32), y.view(torch.int32))
+
+
+ok = True
+g = torch.Generator(device="cuda").manual_seed(7)
+for (h, w) in [(1000, 1024), (517, 384), (300, 4096), (64, 128), (2048, 2048)]:
+    a = torch.rand((h, w), device="cuda", generator=g)
+    b = torch.rand((h, w), device="cuda", generator=g)
+    for kl in (4, 8):
+        last, prev = plain(a, b, h, w, kl)
+        fl, fp = fused(a, b, h, w, kl, (0, h), (0, h))
+        torch.cuda.synchronize()
+        r = same(fl, last) and same(fp, prev)
+        ok &= r
+        print(f"full {h}x{w} KL={kl}: {'bit-identical' if r else 'MISMATCH'}", flush=True)
+        if not r:
+            d = (fl != last).nonzero()
+            print("   first mismatches (last):", d[:5].tolist(), flush=True)
+        # a slab: inputs rows [lo, hi) only, outputs inside the trapezoid
+        lo, hi = h // 4, 3 * h // 4
+        if hi - lo > 2 * kl + 2:
+            fl, fp = fused(a, b, h, w, kl, (lo, hi), (lo + kl, hi - kl))
+            torch.cuda.synchronize()
+            r = same(fl[lo + kl:hi - kl], last[lo + kl:hi - kl]) and same(fp[lo + kl:hi - kl], prev[lo + kl:hi - kl])
+            ok &= r
+            print(f"slab {h}x{w} rows [{lo},{hi}) KL={kl}: {'bit-identical' if r else 'MISMATCH'}", flush=True)
+
+# timing at the BASELINE tile
+h = w = 16384
+a = torch.rand((h, w), device="cuda", generator=g)
+b = torch.rand((h, w), device="cuda", generator=g)
+a2, b2 = torch.empty_like(a), torch.empty_like(a)
+ext = N.box3((0, 0), (h, w))
+box = N.box3((0, 0), (h, w))
+va, vb, va2, vb2 = (view(t, h, w) for t in (a, b, a2, b2))
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+steps = 96
+for rep in range(2):
+    torch.cuda.synchronize()
+    ev[0].record()
+    x, y = va, vb
+    for _ in range(steps):
+        N.call("cq_wave5", 0, 0, N.CQ_F32, ctypes.byref(x), ctypes.byref(y), ctypes.byref(y), ctypes.byref(box),
+               ctypes.byref(ext), C, K2, K4)
+        x, y = y, x
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1])
+    print(f"plain {steps} steps: {ms:.2f} ms = {12 * h * w * steps / ms / 1e6:.0f} GB/s effective", flush=True)
+for kl in (4, 8):
+    for rep in range(2):
+        torch.cuda.synchronize()
+        ev[0].record()
+        src, dst = (va, vb), (va2, vb2)
+        for _ in range(steps // kl):
+            N.call("cq_wave5_fused", 0, 0, kl, ctypes.byref(src[0]), ctypes.byref(src[1]), ctypes.byref(dst[0]),
+                   ctypes.byref(dst[1]), 0, h, 0, h, ctypes.byref(ext), C, K2, K4)
+            src, dst = dst, src
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1])
+        print(f"fused KL={kl} {steps} steps: {ms:.2f} ms = {12 * h * w * steps / ms / 1e6:.0f} GB/s effective "
+              f"({16 * h * w * (steps // kl) / ms / 1e6:.0f} GB/s of 16 B/cell/pass)", flush=True)
+print("ALL OK" if ok else "FAILED", flush=True)
+sys.exit(0 if ok else 1)
