@@ -12,9 +12,13 @@ Buffer/Task/TaskGraph -> generate_commands -> B200 executor.
                (Session.execute(upload=False)), CUDA events, max over ranks.
 * e2e       -- the public call ``run(plan)`` with pinned host input arrays
                (H2D inside the timed region) and the result read back to host.
-* roofline  -- the dominant kernel (cq_wave5 rows kernel): 12 algorithmic
-               bytes per cell per launch / its CUDA-event launch time, against
-               MEASURED_PEAKS.json hbm_gbs.
+* roofline  -- the dominant kernel: the temporally blocked wave pass
+               (cq_wave5_fused, 4 time steps per HBM pass: 16 algorithmic
+               bytes per cell per launch) -- or the one-step kernel (12 B/cell)
+               with CQ_WAVE_FUSE=0 -- over its CUDA-event launch time, against
+               MEASURED_PEAKS.json hbm_gbs.  ``value`` keeps the SURVEY unit
+               (12 B per cell per time step), so with temporal blocking it can
+               exceed the HBM peak.
 * kernels   -- the other BASELINE workloads at this N (SAXPY, N-body, sgemm).
 * energy    -- NVML J/iteration per kernel at the running SM clock.
 
@@ -202,28 +206,42 @@ def bench_wave(args, dist, placement, peaks):
 
     # ---- device-resident value ------------------------------------------
     sess = E.Session(plan, placement, trace=True)
+    if sess.chains:
+        ch = sess.chains[0]
+        execution = (f"temporal blocking (fusion.py): {len(ch.blocks)} out-of-place passes "
+                     f"(KL = {', '.join(str(b.kl) for b in ch.blocks[-2:])} ...) of cq_wave5_fused + "
+                     f"{len(ch.plain)} one-step launches per 100 steps; KL-row halo exchange per pass "
+                     f"(bit-identical to the per-step plan)")
+    else:
+        execution = "one cq_wave5 launch per time step (CQ_WAVE_FUSE=0 or not fusable)"
     sess.execute(upload=True)
     sess.synchronize()
     sess.recycle()
     # one traced replay: per-launch CUDA-event times of every kernel
     sess.execute(upload=False)
     sess.synchronize()
-    wave_launches = [x for x in sess.launch_log if x[0] == "wave5"]
+    # the dominant kernel: the temporally blocked KL=4 pass when the chain is
+    # fused (16 algorithmic B/cell per launch: read X(t), X(t-1), write
+    # X(t+4), X(t+3)), else the one-step kernel (12 B/cell)
+    kinds_seen = {x[0] for x in sess.launch_log}
+    dom_kind = "wave5_fused4" if "wave5_fused4" in kinds_seen else "wave5"
+    bpc = 16 if dom_kind != "wave5" else 12
+    wave_launches = [x for x in sess.launch_log if x[0] == dom_kind]
     launches_per_replay = len(sess.launch_log)
     # dominant launches only: at N > 1 the halo-row launches run concurrently
     # on the boundary stream, so summing every launch would double-count time
     dom_launch = max(wave_launches, key=lambda x: x[1])
     dominant = [x for x in wave_launches if x[1] == dom_launch[1]]
     kern_ms = sum(sess.elapsed_ms(a, b) for _k, _c, _d, _s, a, b in dominant)
-    kern_bytes = sum(12 * cells for _k, cells, *_ in dominant)
+    kern_bytes = sum(bpc * cells for _k, cells, *_ in dominant)
     sess.recycle()
     timing_source = "stream-traced replay"
     if not args.no_graph:
         def select(log):
-            return [x for x in log if x[0] == "wave5" and x[1] == dom_launch[1]]
+            return [x for x in log if x[0] == dom_kind and x[1] == dom_launch[1]]
         g = graph_launch_times(sess, 2, select)
-        if g and "wave5" in g:
-            kern_bytes, kern_ms = 12 * g["wave5"][0], g["wave5"][1]
+        if g and dom_kind in g:
+            kern_bytes, kern_ms = bpc * g[dom_kind][0], g[dom_kind][1]
             timing_source = "timed CUDA-graph replay (event-record nodes)"
     # the timed replays run as one CUDA graph per rank (kernels, copies and
     # NCCL groups captured once), so no per-command host dispatch remains
@@ -294,7 +312,7 @@ def bench_wave(args, dist, placement, peaks):
     finite = bool(np.isfinite(field).all())
 
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "wave5_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "wave5_fused_traffic.json" if bpc == 16 else "wave5_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             t = json.load(fh)
@@ -307,15 +325,18 @@ def bench_wave(args, dist, placement, peaks):
                 "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks[0]["hbm_gbs"], "traffic": traffic,
-                     "kernel": "wave5_rows_kernel<float,32>", "bytes_per_cell": 12,
+                     "kernel": ("wave5_fused_kernel<4,4,6,128> (4 time steps per pass)" if bpc == 16
+                                else "wave5_rows_kernel<float,32>"),
+                     "bytes_per_cell": bpc,
                      "cells_per_launch": dom_launch[1], "launches": len(dominant),
-                     "bytes_per_launch": 12 * dom_launch[1],
+                     "bytes_per_launch": bpc * dom_launch[1],
                      "peak_source": peaks[1] + " hbm_gbs (torch copy)",
                      "launch_timing": timing_source},
         "clocks": clk,
         "gpu_launches": gpu_launches,
         "replay": replay_mode,
         "energy": energy,
+        "execution": execution,
         "H": H, "W": Wd,
     }
 
@@ -493,11 +514,13 @@ def bench_kernels(args, dist, placement, peaks):
         del z
         plan = cq.generate_commands(g, world)
         sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=3, warm=1)
-        wk = kinds.get("wave5", [0, 1.0, 1])
+        fk = "wave5_fused4" if "wave5_fused4" in kinds else "wave5"
+        kb = 16 if fk != "wave5" else esize   # algorithmic bytes per cell per launch
+        wk = kinds.get(fk, [0, 1.0, 1])
         value = esize * rows * args.size * steps * 3 / (ms / 1e3) / 1e9
         out[label] = {"value": value, "unit": "GB/s", "scaling": "weak" if "weak" in label else "strong",
                       "bytes_per_cell": esize, "time_steps": steps, "ms_per_time_step": ms / 3 / steps,
-                      "kernel_gbs_min_rank": dist.min(esize * wk[0] / (wk[1] / 1e3) / 1e9),
+                      "kernel": fk, "kernel_gbs_min_rank": dist.min(kb * wk[0] / (wk[1] / 1e3) / 1e9),
                       "clocks": sess.clocks}
         sess.close()
 
@@ -681,7 +704,7 @@ def main():
                        "parallelism": f"dp{dist.world} (row slabs, one rank per GPU)",
                        "l2": "inputs 2 GiB/GPU >> 126 MB L2 (no flush needed)",
                        "plan_s": wave["plan_s"], "init": "Gaussian pulse (SURVEY.md §8d)",
-                       "replay": wave["replay"]},
+                       "replay": wave["replay"], "execution": wave["execution"]},
             "e2e": wave["e2e"], "roofline": wave["roofline"], "cpu_baseline": cpu,
             "clocks": wave["clocks"], "gpu_launches": wave["gpu_launches"],
             "energy": {"wave5": wave["energy"],

@@ -534,20 +534,40 @@ __global__ void nbody_drift_kernel(const float4* p_in, const float4* __restrict_
 // (out_last) and X(t+KL-1) (out_prev): 16 B/cell per KL steps instead of
 // 12 B/cell per step.  Every intermediate cell is the same DSL tree with the
 // same operands as the one-step kernel (wave_cell order, one rounding per
-// operator, packed FP32x2 lanes are per-lane IEEE RN), so the result is
+// operator; packed FP32x2 lanes are per-lane IEEE RN), so the result is
 // bit-identical to KL launches of wave5_rows_kernel.
 //
-// A warp owns a strip of 128 loaded columns (lane = 4 columns) and emits the
-// middle 128 - 2*KL: level j is exact on columns [j, 128-j) of the strip
-// (west/east neighbours by shuffle; the strip edge loses one column per
+// A warp owns a strip of 32*V loaded columns (lane = V columns) and emits
+// the middle 32*V - 2*KL: level j is exact on columns [j, 32V-j) of the
+// strip (west/east neighbours by shuffle; the strip edge loses one column per
 // level).  It marches RB output rows, loading rows [r0-KL, r1+KL) of the
-// inputs, keeping a 3-row window per level in registers (slot = row mod 3,
-// unrolled so every slot index is static) and prefetching input rows 3
-// ahead.  Global borders clamp exactly like the DSL's ReadView (the border
+// inputs, keeping a 3-row window per level in registers (slot = row mod 3)
+// and a D-row prefetch ring (loop unrolled by lcm so every slot index is
+// static).  Global borders clamp exactly like the DSL's ReadView (the border
 // cell reads itself).  Rows outside [in_lo, in_hi) are not read; the caller
 // keeps [out_lo, out_hi) inside the trapezoid they determine.
-__device__ __forceinline__ float4 wave4_packed(float4 m, float4 n, float4 s, float4 p, float wv, float ev,
-                                               f32x2 c2, f32x2 k22, f32x2 k42) {
+template <int V> struct FVec;
+template <> struct FVec<2> { typedef float2 T; };
+template <> struct FVec<4> { typedef float4 T; };
+
+__device__ __forceinline__ float first_of(float2 v) { return v.x; }
+__device__ __forceinline__ float last_of(float2 v) { return v.y; }
+__device__ __forceinline__ float first_of(float4 v) { return v.x; }
+__device__ __forceinline__ float last_of(float4 v) { return v.w; }
+
+__device__ __forceinline__ float2 wave_vec(float2 m, float2 n, float2 s, float2 p, float wv, float ev, f32x2 c2,
+                                           f32x2 k22, f32x2 k42) {
+  const f32x2 u = pack2(m.x, m.y);
+  const f32x2 lap = sub2(add2(add2(add2(pack2(n.x, n.y), pack2(s.x, s.y)), pack2(wv, m.x)), pack2(m.y, ev)),
+                         mul2(k42, u));
+  const f32x2 o = add2(sub2(mul2(k22, u), pack2(p.x, p.y)), mul2(c2, lap));
+  float2 r;
+  unpack2(o, r.x, r.y);
+  return r;
+}
+
+__device__ __forceinline__ float4 wave_vec(float4 m, float4 n, float4 s, float4 p, float wv, float ev, f32x2 c2,
+                                           f32x2 k22, f32x2 k42) {
   const f32x2 uA = pack2(m.x, m.y), uB = pack2(m.z, m.w);
   const f32x2 mid = pack2(m.y, m.z);  // east of A == west of B
   const f32x2 lapA = sub2(add2(add2(add2(pack2(n.x, n.y), pack2(s.x, s.y)), pack2(wv, m.x)), mid), mul2(k42, uA));
@@ -560,65 +580,86 @@ __device__ __forceinline__ float4 wave4_packed(float4 m, float4 n, float4 s, flo
   return o;
 }
 
-template <int KL, int RB>
-__global__ void __launch_bounds__(256) wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last,
-                                                          cq_view_t out_prev, int64_t in_lo, int64_t in_hi,
-                                                          int64_t out_lo, int64_t out_hi, int64_t H, int64_t W,
-                                                          float c, float k2, float k4) {
-  static_assert(KL >= 2 && KL % 4 == 0, "strip offsets must stay 16-byte aligned");
-  constexpr int SW = 128 - 2 * KL;
-  const int lane = threadIdx.x & 31;
-  const int64_t strip = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+__device__ __forceinline__ void cp_async_row(void* smem, const void* gmem, bool valid, int bytes) {
+  const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int src_size = valid ? bytes : 0;  // 0: zero-fill, source not read
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gmem), "r"(src_size) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(gmem), "r"(src_size) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Input rows stream through a per-warp shared-memory ring D rows deep
+// (cp.async, one commit group per row, each lane fetches and later reads
+// back only its own V columns), so D rows of both inputs are in flight per
+// warp without holding them in registers.
+template <int KL, int V, int D, int RB>
+__global__ void __launch_bounds__(256, 2)
+    wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last, cq_view_t out_prev, int64_t in_lo,
+                       int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, float c, float k2,
+                       float k4) {
+  typedef typename FVec<V>::T Vec;
+  static_assert(KL >= 2 && KL % V == 0, "strip offsets must stay vector aligned");
+  static_assert(D % 3 == 0, "prefetch ring must be a multiple of the window");
+  constexpr int SW = 32 * V - 2 * KL;
+  extern __shared__ __align__(16) uint8_t fused_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Vec* ring = reinterpret_cast<Vec*>(fused_smem) + (size_t)warp * D * 2 * 32;  // [D][2][32]
+  const int64_t strip = (int64_t)blockIdx.x * 8 + warp;
   const int64_t r0 = out_lo + (int64_t)blockIdx.y * RB;
   if (strip * SW >= W || r0 >= out_hi) return;  // warp-uniform
   const int64_t r1 = min(r0 + (int64_t)RB, out_hi);
-  const int64_t col = strip * SW - KL + lane * 4;
+  const int64_t col = strip * SW - KL + lane * V;
   const bool colok = col >= 0 && col < W;
-  const bool keep = lane >= KL / 4 && lane < 32 - KL / 4 && col < W;
-  const bool at_w = col == 0, at_e = col + 4 == W;
+  const bool keep = lane >= KL / V && lane < 32 - KL / V && col < W;
+  const bool at_w = col == 0, at_e = col + V == W;
   const f32x2 c2 = pack2(c, c), k22 = pack2(k2, k2), k42 = pack2(k4, k4);
-  auto ld = [&](const cq_view_t& v, int64_t r) -> float4 {
-    if (!colok || r < in_lo || r >= in_hi) return make_float4(0.f, 0.f, 0.f, 0.f);
-    return __ldcs(reinterpret_cast<const float4*>((const float*)v.ptr + (r - v.alloc.lo[1]) * v.stride[1] +
-                                                  (col - v.alloc.lo[2])));
+  const float* ub = (const float*)u.ptr + (colok ? col : 0) - u.alloc.lo[2];
+  const float* pb = (const float*)upr.ptr + (colok ? col : 0) - upr.alloc.lo[2];
+  auto fetch = [&](int slot, int64_t r) {
+    const bool ok = colok && r >= in_lo && r < in_hi;
+    const int64_t rr = ok ? r : in_lo;
+    cp_async_row(ring + (slot * 2 + 0) * 32 + lane, ub + (rr - u.alloc.lo[1]) * u.stride[1], ok, sizeof(Vec));
+    cp_async_row(ring + (slot * 2 + 1) * 32 + lane, pb + (rr - upr.alloc.lo[1]) * upr.stride[1], ok, sizeof(Vec));
+    cp_async_commit();
   };
-  auto st = [&](const cq_view_t& v, int64_t r, float4 x) {
+  auto st = [&](const cq_view_t& v, int64_t r, Vec x) {
     if (keep && r >= r0 && r < r1)
-      __stcs(reinterpret_cast<float4*>((float*)v.ptr + (r - v.alloc.lo[1]) * v.stride[1] + (col - v.alloc.lo[2])),
-             x);
+      __stcs(reinterpret_cast<Vec*>((float*)v.ptr + (r - v.alloc.lo[1]) * v.stride[1] + (col - v.alloc.lo[2])), x);
   };
-  float4 L[KL][3];  // level j (0 = X(t)) rows, slot = (row - rb) % 3
-  float4 P[3];      // X(t-1) rows
-  float4 Q[3], QP[3];
+  Vec L[KL][3];  // level j (0 = X(t)) rows, slot = (row - rb) % 3
+  Vec P[3];      // X(t-1) rows, same slots
   const int64_t rb = r0 - KL, re = r1 + KL;
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
-    Q[q] = ld(u, rb + q);
-    QP[q] = ld(upr, rb + q);
-  }
+  for (int q = 0; q < D; ++q) fetch(q, rb + q);
 #pragma unroll 1
-  for (int64_t base = rb; base < re; base += 3) {
+  for (int64_t base = rb; base < re; base += D) {
 #pragma unroll
-    for (int s = 0; s < 3; ++s) {
-      const int64_t ri = base + s;
+    for (int sd = 0; sd < D; ++sd) {
+      const int64_t ri = base + sd;
       if (ri < re) {
-        L[0][s] = Q[s];
-        P[s] = QP[s];
-        Q[s] = ld(u, ri + 3);
-        QP[s] = ld(upr, ri + 3);
-        const int so = (s + 1) % 3, sm = (s + 2) % 3;  // slots of rows ri-2, ri-1
+        const int s = sd % 3, so = (sd + 1) % 3, sm = (sd + 2) % 3;  // rows ri, ri-2, ri-1
+        cp_async_wait<D - 1>();  // row ri (the oldest group) has landed
+        L[0][s] = ring[(sd * 2 + 0) * 32 + lane];
+        P[s] = ring[(sd * 2 + 1) * 32 + lane];
+        fetch(sd, ri + D);
 #pragma unroll
         for (int j = 1; j <= KL; ++j) {
           const int64_t rho = ri - j;
-          const float4 mid = L[j - 1][sm];
-          const float4 nn = (rho == 0) ? mid : L[j - 1][so];
-          const float4 ss = (rho == H - 1) ? mid : L[j - 1][s];
-          const float4 pp = (j == 1) ? P[sm] : L[j >= 2 ? j - 2 : 0][so];
-          float wv = __shfl_up_sync(0xffffffffu, mid.w, 1);
-          float ev = __shfl_down_sync(0xffffffffu, mid.x, 1);
-          if (at_w) wv = mid.x;
-          if (at_e) ev = mid.w;
-          const float4 o = wave4_packed(mid, nn, ss, pp, wv, ev, c2, k22, k42);
+          const Vec mid = L[j - 1][sm];
+          const Vec nn = (rho == 0) ? mid : L[j - 1][so];
+          const Vec ss = (rho == H - 1) ? mid : L[j - 1][s];
+          const Vec pp = (j == 1) ? P[sm] : L[j >= 2 ? j - 2 : 0][so];
+          float wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
+          float ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
+          if (at_w) wv = first_of(mid);
+          if (at_e) ev = last_of(mid);
+          const Vec o = wave_vec(mid, nn, ss, pp, wv, ev, c2, k22, k42);
           if (j < KL) L[j][s] = o;
           if (j == KL - 1) st(out_prev, rho, o);
           if (j == KL) st(out_last, rho, o);
@@ -626,6 +667,7 @@ __global__ void __launch_bounds__(256) wave5_fused_kernel(cq_view_t u, cq_view_t
       }
     }
   }
+  cp_async_wait<0>();
 }
 
 }  // namespace cq
@@ -743,15 +785,37 @@ int cq_wave5_fused(int device, int stream, int levels, const cq_view_t* u, const
              "cq_wave5_fused: rows [%lld, %lld) are not determined by input rows [%lld, %lld)",
              (long long)out_lo, (long long)out_hi, (long long)in_lo, (long long)in_hi);
   constexpr int RB = 128;
-  const int sw = 128 - 2 * levels;
+  static int variant = [] {
+    const char* e = getenv("CQ_WAVE_FUSED_V");
+    return e ? atoi(e) : 4;
+  }();
+  const int vw = variant == 2 ? 2 : 4;
+  const int sw = 32 * vw - 2 * levels;
   const int64_t strips = (W + sw - 1) / sw;
   dim3 grid((unsigned)((strips + 7) / 8), (unsigned)((out_hi - out_lo + RB - 1) / RB));
-  if (levels == 4)
-    wave5_fused_kernel<4, RB><<<grid, 256, 0, st>>>(*u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H,
-                                                    W, (float)c, (float)k2, (float)k4);
-  else
-    wave5_fused_kernel<8, RB><<<grid, 256, 0, st>>>(*u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H,
-                                                    W, (float)c, (float)k2, (float)k4);
+  static int depth = [] {
+    const char* e = getenv("CQ_WAVE_FUSED_D");
+    return e ? atoi(e) : 12;
+  }();
+#define CQ_FUSED(KL, VV, DD)                                                                                 \
+  do {                                                                                                       \
+    auto kern = wave5_fused_kernel<KL, VV, DD, RB>;                                                          \
+    const int smem = 8 * DD * 2 * 32 * VV * 4;                                                               \
+    CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));            \
+    kern<<<grid, 256, smem, st>>>(*u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H, W, (float)c, \
+                                  (float)k2, (float)k4);                                                      \
+  } while (0)
+  if (vw == 2) {
+    if (levels == 4) CQ_FUSED(4, 2, 12);
+    else CQ_FUSED(8, 2, 12);
+  } else if (depth == 6) {
+    if (levels == 4) CQ_FUSED(4, 4, 6);
+    else CQ_FUSED(8, 4, 6);
+  } else {
+    if (levels == 4) CQ_FUSED(4, 4, 12);
+    else CQ_FUSED(8, 4, 12);
+  }
+#undef CQ_FUSED
   CQ_CHECK_LAUNCH();
   return CQ_OK;
 }

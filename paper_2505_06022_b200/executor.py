@@ -40,7 +40,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native as N
-from . import jit
+from . import fusion, jit
 from .errors import EvalError, MapperViolationError, NativeError, ValidationError
 from .lowering import bind_task
 from .model import AccessMode, NativeKernel, apply_mapper
@@ -319,21 +319,22 @@ class _View:
 # ------------------------------------------------------------- hazard tracker
 
 class _Hazards:
-    """Per (node, buffer) list of recent accesses -> events to wait on.
+    """Per physical allocation list of recent accesses -> events to wait on.
 
-    An access is (region, write?, stream key, event).  A new op on stream S
-    waits for every conflicting access (RAW, WAR, WAW) issued on another
-    stream; same-stream order is implicit.  Entries covered by a newer write,
-    or by a newer access on the same stream, can never be the binding
-    constraint again and are dropped."""
+    An access is (key, region, write?) with key = the allocation (a view's
+    id, so the alternate arrays of a fused wave chain are tracked apart even
+    as they swap roles).  A new op on stream S waits for every conflicting
+    access (RAW, WAR, WAW) issued on another stream; same-stream order is
+    implicit.  Entries covered by a newer write, or by a newer access on the
+    same stream, can never be the binding constraint again and are dropped."""
 
     def __init__(self):
         self.log = {}
 
     def waits(self, accesses, skey):
         out = {}
-        for node, buf, region, write in accesses:
-            for r, w, sk, ev in self.log.get((node, buf), ()):
+        for key, region, write in accesses:
+            for r, w, sk, ev in self.log.get(key, ()):
                 if sk == skey or not (write or w):
                     continue
                 if region.overlaps(r):
@@ -341,8 +342,7 @@ class _Hazards:
         return out
 
     def record(self, accesses, skey, event):
-        for node, buf, region, write in accesses:
-            key = (node, buf)
+        for key, region, write in accesses:
             kept = []
             for entry in self.log.get(key, ()):
                 r, w, sk, ev = entry
@@ -420,6 +420,8 @@ class Session:
         for d in self.devices:
             N.call("cq_init_device", d)
         kahn_order(plan)  # validates acyclicity before touching devices
+        self.alt = {}
+        self.chains = fusion.find_chains(plan, self._raw_schedule())
         self.allocate()
         self.pin_inputs()
 
@@ -462,6 +464,7 @@ class Session:
         """Run ``fn`` on (device, stream) after the hazards it depends on.
         Returns (start, stop) events; ``start`` is None unless tracing."""
         skey = (device, stream)
+        accesses = self._keyed(accesses)
         for ev, _sk in self.haz.waits(accesses, skey).items():
             N.call("cq_stream_wait_event", device, stream, ctypes.c_uint64(ev))
         start = tstop = None
@@ -478,6 +481,20 @@ class Session:
         N.call("cq_event_record", ctypes.c_uint64(stop), device, stream)
         self.haz.record(accesses, skey, stop)
         return start, tstop or stop
+
+    def _keyed(self, accesses):
+        """(node, buffer, region, write) -> (allocation key, region, write) for
+        the node's current view; (view, region, write) names a view directly."""
+        out = []
+        for acc in accesses:
+            if len(acc) == 3:
+                view, region, write = acc
+                out.append((id(view), region, write))
+            else:
+                node, buf, region, write = acc
+                v = self.views.get((node, buf))
+                out.append((id(v) if v is not None else (node, buf), region, write))
+        return out
 
     # ---- allocation ----------------------------------------------------
     def allocate(self):
@@ -502,6 +519,14 @@ class Session:
                     continue  # gathered straight from the host array
                 for h in holders:
                     touch.setdefault((h, name), []).append(reg.bounding_box())
+        fused = set()
+        for ch in self.chains:
+            # fused blocks read a KL-deep halo and write out of place
+            for node, (lo, hi) in ch.rows.items():
+                for buf in (ch.a, ch.b):
+                    touch.setdefault((node, buf), []).append(
+                        Box((max(lo - ch.depth, 0), 0), (min(hi + ch.depth, ch.H), ch.W)))
+                    fused.add((node, buf))
         for (node, buf), boxes in sorted(touch.items()):
             if not self.local(node):
                 continue
@@ -510,6 +535,8 @@ class Session:
                 continue
             b = self.buffers[buf]
             self.views[(node, buf)] = _View(node, self.dev(node), buf, bb, b.itemsize)
+            if (node, buf) in fused:
+                self.alt[(node, buf)] = _View(node, self.dev(node), buf, bb, b.itemsize)
 
     # ---- host-initialised data -----------------------------------------
     def host_array(self, buf):
@@ -663,7 +690,7 @@ class Session:
 
     # ---- timing marks for the trace ----------------------------------------
     def mark_transfer(self, push, node, events):
-        if self.want_trace:
+        if self.want_trace and push.id is not None:
             start, stop = events
             self.trace_marks.append((push, node, self.dev(node), start, stop))
 
@@ -720,6 +747,53 @@ class Session:
                 self.launch_log.append((kind, box.volume(), dev, stream, t[0], t[1]))
         if self.want_trace:
             self.trace_marks.append((cmd, node, dev, marks, None))
+
+    def exec_fused(self, ch, block, hostinit):
+        """One temporally blocked wave block (fusion.py): the KL-row halo
+        exchange, then per local node the interior launch (compute stream)
+        and the neighbour-edge launches (boundary stream, after the
+        exchange), all out of place; the alternates then become current."""
+        kl = block.kl
+        if hostinit:
+            self.flush_group(hostinit)   # upload-time materialisation only
+        b = self.buffers[ch.a]
+        self.flush_group(fusion.halo_pushes(ch, kl, b.itemsize))
+        ext = _cbox(b.extent)
+        W = ch.W
+        if not hasattr(self, "_exec_of"):
+            self._exec_of = {(c.task_id, c.node): c for c in self.plan.commands if isinstance(c, ExecuteCommand)}
+        for node in sorted(ch.rows):
+            if not self.local(node):
+                continue
+            dev = self.dev(node)
+            ua, pb = self.views[(node, ch.a)], self.views[(node, ch.b)]
+            oa, ob = self.alt[(node, ch.a)], self.alt[(node, ch.b)]
+            marks = []
+            interior, edge_t, edge_b = fusion.node_ranges(ch, node, kl)
+            for rng, stream in ((interior, N.STREAM_COMPUTE), (edge_t, N.STREAM_BOUNDARY),
+                                (edge_b, N.STREAM_BOUNDARY)):
+                if rng is None or rng[3] <= rng[2]:
+                    continue
+                in_lo, in_hi, out_lo, out_hi = rng
+                rin = Region.from_box(Box((in_lo, 0), (in_hi, W)))
+                rout = Region.from_box(Box((out_lo, 0), (out_hi, W)))
+                acc = [(ua, rin, False), (pb, rin, False), (oa, rout, True), (ob, rout, True)]
+
+                def go(stream=stream, rng=rng):
+                    N.call("cq_wave5_fused", dev, stream, kl, ctypes.byref(ua.c), ctypes.byref(pb.c),
+                           ctypes.byref(oa.c), ctypes.byref(ob.c), rng[0], rng[1], rng[2], rng[3],
+                           ctypes.byref(ext), ctypes.c_double(ch.c), ctypes.c_double(ch.k2),
+                           ctypes.c_double(ch.k4))
+                t = self.issue(dev, stream, acc, go)
+                marks.append(t)
+                if self.want_trace:
+                    self.launch_log.append((f"wave5_fused{kl}", (out_hi - out_lo) * W, dev, stream, t[0], t[1]))
+            # X(t+KL) / X(t+KL-1) now live in the alternates
+            self.views[(node, ch.a)], self.alt[(node, ch.a)] = oa, ua
+            self.views[(node, ch.b)], self.alt[(node, ch.b)] = ob, pb
+            if self.want_trace:
+                for i, tid in enumerate(block.tasks):
+                    self.trace_marks.append((self._exec_of[(tid, node)], node, dev, marks, (i, kl)))
 
     def split(self, task, cmd, awaited):
         """Cut the chunk along dim 0 into rows that do not read awaited
@@ -911,10 +985,15 @@ class Session:
 
     # ---- the walk --------------------------------------------------------
     def schedule(self):
-        """Global transfer groups and per-execute awaited regions (identical
-        on every rank; computed once per session)."""
-        if self._sched is not None:
-            return self._sched
+        """Global transfer groups and per-execute awaited regions, with fused
+        wave blocks substituted (identical on every rank; computed once)."""
+        if self._sched is None:
+            self._sched = fusion.transform(self._raw_schedule(), self.chains)
+        return self._sched
+
+    def _raw_schedule(self):
+        if getattr(self, "_raw", None) is not None:
+            return self._raw
         # Task-major order: every push of a task depends only on commands of
         # earlier tasks (producers are read from the table state before the
         # task, scheduler.py:263-314), so all of a task's pushes can be posted
@@ -957,7 +1036,7 @@ class Session:
                     if isinstance(a, AwaitPushCommand) and a.dst == c.node:
                         aw[a.buffer] = aw[a.buffer].union(a.region) if a.buffer in aw else a.region
                 steps.append(("exec", c, aw))
-        self._sched = steps
+        self._raw = steps
         return steps
 
     def execute(self, upload: bool = True):
@@ -980,6 +1059,8 @@ class Session:
         for step in self.schedule():
             if step[0] == "group":
                 self.flush_group(step[1])
+            elif step[0] == "fused":
+                self.exec_fused(*step[1:])
             elif self.local(step[1].node):
                 self.exec_command(step[1], step[2])
 
@@ -1265,12 +1346,16 @@ class Session:
         for item in self.trace_marks:
             cmd = item[0]
             if isinstance(cmd, ExecuteCommand):
-                _c, node, dev, marks, _ = item
+                _c, node, dev, marks, share = item
                 starts = [secs(dev, a) for a, _b in marks]
                 stops = [secs(dev, b) for _a, b in marks]
                 if not starts:
                     continue
                 t0, t1 = min(starts), max(stops)
+                if share is not None:
+                    # one of KL steps of a fused block: an equal slice of it
+                    i, kl = share
+                    t0, t1 = t0 + (t1 - t0) * i / kl, t0 + (t1 - t0) * (i + 1) / kl
                 task = self.plan.graph.task(cmd.task_id)
                 trace.append(TraceEvent("execute", node, cmd.id, t0, t1 - t0,
                                         frequency_ghz=cmd.frequency_ghz, task_id=cmd.task_id,
@@ -1288,8 +1373,9 @@ class Session:
         return trace, makespan
 
     def release(self):
-        for v in self.views.values():
+        for v in list(self.views.values()) + list(self.alt.values()):
             v.free()
+        self.alt.clear()
         for dev, item in self.scratch:
             if isinstance(item, _View):
                 item.free()

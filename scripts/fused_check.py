@@ -78,10 +78,33 @@ a2, b2 = torch.empty_like(a), torch.empty_like(a)
 ext = N.box3((0, 0), (h, w))
 box = N.box3((0, 0), (h, w))
 va, vb, va2, vb2 = (view(t, h, w) for t in (a, b, a2, b2))
-ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+
+class Ev:
+    """cq timing event on the compute stream (the kernels' stream, not torch's)."""
+    def __init__(self):
+        h = ctypes.c_uint64()
+        N.call("cq_event_create", 0, 1, ctypes.byref(h))
+        self.h = h.value
+
+    def record(self):
+        N.call("cq_event_record", ctypes.c_uint64(self.h), 0, 0)
+
+    def elapsed_time(self, other):
+        ms = ctypes.c_float()
+        N.call("cq_event_elapsed_ms", ctypes.c_uint64(self.h), ctypes.c_uint64(other.h), ctypes.byref(ms))
+        return ms.value
+
+
+def sync():
+    N.call("cq_stream_synchronize", 0, 0)
+
+
+ev = [Ev(), Ev()]
 steps = 96
 for rep in range(2):
     torch.cuda.synchronize()
+    sync()
     ev[0].record()
     x, y = va, vb
     for _ in range(steps):
@@ -89,12 +112,13 @@ for rep in range(2):
                ctypes.byref(ext), C, K2, K4)
         x, y = y, x
     ev[1].record()
-    torch.cuda.synchronize()
+    sync()
     ms = ev[0].elapsed_time(ev[1])
     print(f"plain {steps} steps: {ms:.2f} ms = {12 * h * w * steps / ms / 1e6:.0f} GB/s effective", flush=True)
 for kl in (4, 8):
     for rep in range(2):
         torch.cuda.synchronize()
+        sync()
         ev[0].record()
         src, dst = (va, vb), (va2, vb2)
         for _ in range(steps // kl):
@@ -102,7 +126,7 @@ for kl in (4, 8):
                    ctypes.byref(dst[1]), 0, h, 0, h, ctypes.byref(ext), C, K2, K4)
             src, dst = dst, src
         ev[1].record()
-        torch.cuda.synchronize()
+        sync()
         ms = ev[0].elapsed_time(ev[1])
         print(f"fused KL={kl} {steps} steps: {ms:.2f} ms = {12 * h * w * steps / ms / 1e6:.0f} GB/s effective "
               f"({16 * h * w * (steps // kl) / ms / 1e6:.0f} GB/s of 16 B/cell/pass)", flush=True)

@@ -1,0 +1,19 @@
+"""One cq_wave5_fused launch at 16384^2 (for ncu)."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from paper_2505_06022_b200 import _native as N  # noqa: E402
+N.call("cq_init_device", 0)
+kl = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+h = w = 16384
+t = [torch.rand((h, w), device="cuda") for _ in range(4)]
+torch.cuda.synchronize()
+def view(x):
+    v = N.CqView(); v.ptr = x.data_ptr(); v.alloc = N.box3((0, 0), (h, w)); v.stride[:] = [h * w, w, 1]; return v
+vs = [view(x) for x in t]
+ext = N.box3((0, 0), (h, w))
+for i in range(3):
+    N.call("cq_wave5_fused", 0, 0, kl, ctypes.byref(vs[0]), ctypes.byref(vs[1]), ctypes.byref(vs[2]),
+           ctypes.byref(vs[3]), 0, h, 0, h, ctypes.byref(ext), 0.25, 2.0, 4.0)
+N.call("cq_stream_synchronize", 0, 0)
+print("ok")

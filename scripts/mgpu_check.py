@@ -38,16 +38,21 @@ def main():
     from oracle import native as onat
 
     # wave ping-pong, nodes = world and 2*world - 1 (uneven slabs)
-    h, w, steps = 515, 384, 9
+    # (temporally blocked when the chain is >= 8 steps: KL-row halo exchange
+    # between ranks; CQ_WAVE_FUSE=0 runs the per-step plan)
+    h, w = 515, 384
     u0 = np.random.default_rng(2).uniform(0, 1, (h, w)).astype(np.float32)
     up0 = np.random.default_rng(3).uniform(0, 1, (h, w)).astype(np.float32)
-    for nodes in sorted({world, max(1, 2 * world - 1)}):
-        prog = W.wave_program(h, w, steps=steps, kind="float32", u0=u0, up0=up0)
-        res = E.run(cq.generate_commands(prog.graph(), nodes), placement=pl)
-        if rank == 0:
-            u, up = onat.wave_run(u0, up0, steps, 0.25)
-            check(f"wave {h}x{w}x{steps} nodes={nodes}",
-                  dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up))
+    for steps, fuse in ((9, "1"), (9, "0"), (22, "1")):
+        os.environ["CQ_WAVE_FUSE"] = fuse
+        for nodes in sorted({world, max(1, 2 * world - 1)}):
+            prog = W.wave_program(h, w, steps=steps, kind="float32", u0=u0, up0=up0)
+            res = E.run(cq.generate_commands(prog.graph(), nodes), placement=pl)
+            if rank == 0:
+                u, up = onat.wave_run(u0, up0, steps, 0.25)
+                check(f"wave {h}x{w}x{steps} nodes={nodes} fuse={fuse}",
+                      dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up))
+    os.environ.pop("CQ_WAVE_FUSE")
 
     # SAXPY, BASELINE config 1 shape scaled
     n = (1 << 22) + 5

@@ -269,6 +269,33 @@ class FakeLib:
         self.launches.append("wave5")
         return 0
 
+    def cq_wave5_fused(self, d, s, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi, ext, c, k2,
+                       k4):
+        """KL ping-pong steps on rows [in_lo, in_hi) (edge rows replicate,
+        which is exact at the true borders and only spoils rows outside the
+        trapezoid), then rows [out_lo, out_hi) of the last two levels."""
+        u, upr, ol, op, e = (_obj(x) for x in (u, upr, out_last, out_prev, ext))
+        in_lo, in_hi, out_lo, out_hi, levels = (_val(x) for x in (in_lo, in_hi, out_lo, out_hi, levels))
+        dt = np.float32
+        W = e.hi[2]
+        box = N.box3((in_lo, 0), (in_hi, W))
+        cur = self._view(u, dt, box)[0].copy()
+        prev = self._view(upr, dt, box)[0].copy()
+        c, k2, k4 = dt(_val(c)), dt(_val(k2)), dt(_val(k4))
+        cols = np.arange(W)
+        for _ in range(levels):
+            n = cur[np.clip(np.arange(cur.shape[0]) - 1, 0, cur.shape[0] - 1)]
+            sth = cur[np.clip(np.arange(cur.shape[0]) + 1, 0, cur.shape[0] - 1)]
+            w = cur[:, np.clip(cols - 1, 0, W - 1)]
+            east = cur[:, np.clip(cols + 1, 0, W - 1)]
+            lap = (((n + sth) + w) + east) - k4 * cur
+            cur, prev = ((k2 * cur) - prev) + c * lap, cur
+        ob = N.box3((out_lo, 0), (out_hi, W))
+        self._view(ol, dt, ob)[0][...] = cur[out_lo - in_lo:out_hi - in_lo]
+        self._view(op, dt, ob)[0][...] = prev[out_lo - in_lo:out_hi - in_lo]
+        self.launches.append("wave5_fused")
+        return 0
+
     def cq_expr_eval(self, d, s, X):
         X = _obj(X)
         dt = _DT[X.kind]
@@ -448,7 +475,7 @@ def _graph_api(cls):
     cls.cq_graph_begin, cls.cq_graph_end = begin, end
     cls.cq_graph_launch, cls.cq_graph_destroy = launch, destroy
     # wrap kernel entry points so they are recorded while capturing
-    for name in ("cq_saxpy", "cq_wave5", "cq_expr_eval", "cq_fill", "cq_copy_box", "cq_pack_box",
+    for name in ("cq_saxpy", "cq_wave5", "cq_wave5_fused", "cq_expr_eval", "cq_fill", "cq_copy_box", "cq_pack_box",
                  "cq_unpack_box", "cq_nbody_kick", "cq_nbody_drift", "cq_sgemm"):
         fn = getattr(cls, name)
 

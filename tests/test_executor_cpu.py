@@ -143,6 +143,18 @@ def _rank_main(rank, world, port, outdir):
             results[f"wave{nodes}_up"] = res.buffers["up"]
         loc = E.run(cq.generate_commands(prog.graph(), nodes), placement=pl, gather="local")
         results[f"local{nodes}_r{rank}"] = loc.buffers.get("u", np.zeros(0))
+    # temporally blocked chain: the KL-row halo exchange crosses ranks
+    fu0 = np.random.default_rng(10).uniform(0, 1, (160, 32)).astype(np.float32)
+    for nodes in (2, 3):
+        prog = W.wave_program(160, 32, steps=14, kind="float32", u0=fu0, up0=fu0)
+        sess = E.Session(cq.generate_commands(prog.graph(), nodes), pl)
+        assert [b.kl for b in sess.chains[0].blocks] == [4, 8]
+        sess.execute(upload=True)
+        sess.synchronize()
+        res = sess.results()
+        sess.close()
+        if rank == 0:
+            results[f"fwave{nodes}_u"], results[f"fwave{nodes}_up"] = res["u"], res["up"]
     for idx in OK_IDX[::6]:
         entry = PROGRAMS[idx]
         buffers, tasks = program_from_json(entry["program"])
@@ -177,6 +189,10 @@ def test_two_ranks_gloo(tmp_path):
     u, up = onat.wave_run(u0, u0, 5, 0.25)
     for nodes in (2, 3):
         assert dsl.same_bits(r0[f"wave{nodes}_u"], u) and dsl.same_bits(r0[f"wave{nodes}_up"], up)
+    fu0 = np.random.default_rng(10).uniform(0, 1, (160, 32)).astype(np.float32)
+    fu, fup = onat.wave_run(fu0, fu0, 14, 0.25)
+    for nodes in (2, 3):
+        assert dsl.same_bits(r0[f"fwave{nodes}_u"], fu) and dsl.same_bits(r0[f"fwave{nodes}_up"], fup)
     # gather="local": each rank holds exactly its own final rows
     assert dsl.same_bits(r0["local2_r0"][:19], u[:19]) and dsl.same_bits(r1["local2_r1"][19:], u[19:])
     for key, val in r0.items():
@@ -220,3 +236,66 @@ def test_graph_capture_replays_same_commands(fake):
     assert lib.launches.count("wave5") == 4 * base
     s.close()
     assert s.graph is None and s.graph_events == []
+
+
+# ------------------------------------------- temporally blocked wave chains
+
+@pytest.mark.parametrize("steps,nodes,ndev", [(22, 1, 1), (22, 3, 1), (16, 4, 2), (9, 2, 1), (100, 3, 2)])
+def test_fused_wave_chain_matches_oracle(fake, monkeypatch, steps, nodes, ndev):
+    """Fused blocks (KL=4 and a parity KL=8 block) + plain leftovers give the
+    per-step result bit for bit, with nodes sharing or spanning devices."""
+    from paper_2505_06022_b200 import fusion
+    from oracle import native as onat
+    lib = fake(ndev)
+    h, w = 200, 64
+    u0 = np.random.default_rng(11).uniform(0, 1, (h, w)).astype(np.float32)
+    up0 = np.random.default_rng(12).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=steps, kind="float32", u0=u0, up0=up0)
+    plan = cq.generate_commands(prog.graph(), nodes)
+    s = E.Session(plan, E.Placement(1, 0, tuple(range(ndev))))
+    assert (len(s.chains) == 1) == (steps >= 8)
+    if s.chains:
+        ch = s.chains[0]
+        assert len(ch.blocks) % 2 == 0
+        assert sum(b.kl for b in ch.blocks) + len(ch.plain) == steps
+    s.execute(upload=True)
+    s.synchronize()
+    res = s.results()
+    trace, _ = s.trace()
+    s.close()
+    u, up = onat.wave_run(u0, up0, steps, 0.25)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+    if steps >= 8:
+        assert "wave5_fused" in lib.launches
+    # one trace event per execute command, fused or not
+    assert sum(1 for e in trace if e.kind == "execute") == steps * nodes
+
+
+def test_fused_chain_disabled_and_graph_replay(fake, monkeypatch):
+    from oracle import native as onat
+    lib = fake(1)
+    h, w, steps = 160, 32, 12
+    u0 = np.random.default_rng(5).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=steps, kind="float32", u0=u0, up0=u0)
+    plan = cq.generate_commands(prog.graph(), 2)
+    monkeypatch.setenv("CQ_WAVE_FUSE", "0")
+    s0 = E.Session(plan, E.Placement(1, 0, (0,)))
+    assert s0.chains == []
+    s0.close()
+    monkeypatch.delenv("CQ_WAVE_FUSE")
+    s = E.Session(plan, E.Placement(1, 0, (0,)))
+    assert [b.kl for b in s.chains[0].blocks] == [4, 8]
+    s.execute(upload=True)
+    s.synchronize()
+    s.recycle()
+    views0 = {k: v.ptr for k, v in s.views.items()}
+    s.capture()
+    # an even number of out-of-place blocks: the captured replay starts and
+    # ends on the same allocations
+    assert {k: v.ptr for k, v in s.views.items()} == views0
+    s.replay(2)
+    s.synchronize()
+    res = s.results()
+    s.close()
+    u, up = onat.wave_run(u0, u0, 3 * steps, 0.25)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)

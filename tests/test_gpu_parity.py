@@ -124,6 +124,59 @@ def test_wave_bit_exact_vs_oracle(nodes, kind):
     assert dsl.same_bits(res.buffers["up"], up)
 
 
+@pytest.mark.parametrize("nodes,steps", [(1, 22), (1, 100), (3, 22), (4, 36), (2, 9)])
+def test_fused_wave_chain_bit_exact_vs_oracle(nodes, steps):
+    """Temporal blocking (cq_wave5_fused: KL=4 blocks, one KL=8 parity
+    block, KL-row halo exchange between slabs, plain leftovers) reproduces
+    the per-step oracle bit for bit."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    h, w = 515, 640
+    u0 = np.random.default_rng(21).uniform(0, 1, (h, w)).astype(np.float32)
+    up0 = np.random.default_rng(22).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=steps, kind="float32", c=0.25, u0=u0, up0=up0)
+    s = Session(cq.generate_commands(prog.graph(), nodes), Placement(1, 0, (0,)))
+    assert len(s.chains) == 1
+    s.execute(upload=True)
+    s.synchronize()
+    res = s.results()
+    kinds = {k for k, *_ in s.launch_log}
+    s.close()
+    assert any(k.startswith("wave5_fused") for k in kinds)
+    u, up = onat.wave_run(u0, up0, steps, 0.25)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
+def test_fused_wave_graph_replay_continues_the_simulation():
+    """A captured fused execution replayed twice == two more plain fused
+    executions == the 3x-longer simulation (the KL-row exchange makes a
+    re-execution on resident data a true continuation; an even number of
+    out-of-place blocks keeps the captured pointers valid)."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    h, w, steps = 384, 512, 26
+    u0 = np.random.default_rng(23).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=steps, kind="float32", u0=u0, up0=u0)
+    plan = cq.generate_commands(prog.graph(), 2)
+    out = []
+    for graph in (False, True):
+        s = Session(plan, Placement(1, 0, (0,)))
+        assert s.chains
+        s.execute(upload=True)
+        s.synchronize()
+        s.recycle()
+        if graph:
+            s.capture()
+            s.replay(2)
+        else:
+            for _ in range(2):
+                s.execute(upload=False)
+        s.synchronize()
+        out.append(s.results())
+        s.close()
+    u, up = onat.wave_run(u0, u0, 3 * steps, 0.25)
+    for o in out:
+        assert dsl.same_bits(o["u"], u) and dsl.same_bits(o["up"], up)
+
+
 def test_wave_unaligned_width_uses_generic_kernel():
     h, w = 64, 37
     u0 = np.random.default_rng(3).uniform(0, 1, (h, w)).astype(np.float32)
