@@ -670,6 +670,20 @@ __global__ void __launch_bounds__(256, 2)
   cp_async_wait<0>();
 }
 
+template <int KL, int V, int D, int RB>
+static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& upr, const cq_view_t& ol,
+                        const cq_view_t& op, int64_t in_lo, int64_t in_hi, int64_t out_lo, int64_t out_hi,
+                        int64_t H, int64_t W, float c, float k2, float k4) {
+  constexpr int sw = 32 * V - 2 * KL;
+  const int64_t strips = (W + sw - 1) / sw;
+  dim3 grid((unsigned)((strips + 7) / 8), (unsigned)((out_hi - out_lo + RB - 1) / RB));
+  auto kern = wave5_fused_kernel<KL, V, D, RB>;
+  const int smem = 8 * D * 2 * 32 * V * (int)sizeof(float);
+  CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, 256, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4);
+  return CQ_OK;
+}
+
 }  // namespace cq
 
 using namespace cq;
@@ -784,38 +798,32 @@ int cq_wave5_fused(int device, int stream, int levels, const cq_view_t* u, const
   CQ_REQUIRE(out_lo >= lo_ok && out_hi <= hi_ok && in_lo >= 0 && in_hi <= H,
              "cq_wave5_fused: rows [%lld, %lld) are not determined by input rows [%lld, %lld)",
              (long long)out_lo, (long long)out_hi, (long long)in_lo, (long long)in_hi);
-  constexpr int RB = 128;
-  static int variant = [] {
-    const char* e = getenv("CQ_WAVE_FUSED_V");
-    return e ? atoi(e) : 4;
+  // tuning: CQ_WAVE_FUSED_CFG="V,D,RB" (lane width, cp.async ring depth,
+  // rows per warp segment); default 4,6,128
+  static int cfg = [] {
+    int v = 4, d = 6, rb = 128;
+    if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d,%d", &v, &d, &rb);
+    return v * 10000 + d * 1000 + rb;
   }();
-  const int vw = variant == 2 ? 2 : 4;
-  const int sw = 32 * vw - 2 * levels;
-  const int64_t strips = (W + sw - 1) / sw;
-  dim3 grid((unsigned)((strips + 7) / 8), (unsigned)((out_hi - out_lo + RB - 1) / RB));
-  static int depth = [] {
-    const char* e = getenv("CQ_WAVE_FUSED_D");
-    return e ? atoi(e) : 12;
-  }();
-#define CQ_FUSED(KL, VV, DD)                                                                                 \
-  do {                                                                                                       \
-    auto kern = wave5_fused_kernel<KL, VV, DD, RB>;                                                          \
-    const int smem = 8 * DD * 2 * 32 * VV * 4;                                                               \
-    CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));            \
-    kern<<<grid, 256, smem, st>>>(*u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H, W, (float)c, \
-                                  (float)k2, (float)k4);                                                      \
-  } while (0)
-  if (vw == 2) {
-    if (levels == 4) CQ_FUSED(4, 2, 12);
-    else CQ_FUSED(8, 2, 12);
-  } else if (depth == 6) {
-    if (levels == 4) CQ_FUSED(4, 4, 6);
-    else CQ_FUSED(8, 4, 6);
-  } else {
-    if (levels == 4) CQ_FUSED(4, 4, 12);
-    else CQ_FUSED(8, 4, 12);
+  int status;
+  switch (cfg * 10 + levels) {
+#define CQ_FUSED_CASE(VV, DD, RBB, KL)                                                               \
+  case (VV * 10000 + DD * 1000 + RBB) * 10 + KL:                                                   \
+    status = launch_fused<KL, VV, DD, RBB>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H, W, \
+                                           (float)c, (float)k2, (float)k4);                       \
+    break;
+    CQ_FUSED_CASE(4, 6, 128, 4) CQ_FUSED_CASE(4, 6, 128, 8)
+    CQ_FUSED_CASE(4, 6, 256, 4) CQ_FUSED_CASE(4, 6, 256, 8)
+    CQ_FUSED_CASE(4, 9, 256, 4) CQ_FUSED_CASE(4, 9, 256, 8)
+    CQ_FUSED_CASE(4, 12, 128, 4) CQ_FUSED_CASE(4, 12, 128, 8)
+    CQ_FUSED_CASE(4, 12, 256, 4) CQ_FUSED_CASE(4, 12, 256, 8)
+    CQ_FUSED_CASE(2, 12, 128, 4) CQ_FUSED_CASE(2, 12, 128, 8)
+#undef CQ_FUSED_CASE
+    default:
+      set_error("cq_wave5_fused: CQ_WAVE_FUSED_CFG=%d not compiled", cfg);
+      return CQ_ERR_ARG;
   }
-#undef CQ_FUSED
+  if (status != CQ_OK) return status;
   CQ_CHECK_LAUNCH();
   return CQ_OK;
 }

@@ -564,7 +564,7 @@ class Session:
                     arr = self.host_array(buf)
                     if _needs_bounce(arr, box):
                         sl = tuple(slice(lo, hi) for lo, hi in zip(box.mins, box.maxs))
-                        tmp = np.ascontiguousarray(arr[sl])
+                        tmp = np.array(arr[sl], copy=True)  # never a view of the pinned array
                         self.bounce.append(tmp)
                         N.call("cq_copy_box_h2d", dev, stream, b.itemsize, ctypes.byref(view.c),
                                ctypes.c_void_p(tmp.ctypes.data), ctypes.byref(cb), ctypes.byref(cb))

@@ -299,3 +299,28 @@ def test_fused_chain_disabled_and_graph_replay(fake, monkeypatch):
     s.close()
     u, up = onat.wave_run(u0, u0, 3 * steps, 0.25)
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
+def test_partially_pinned_input_is_bounced_through_a_copy(fake, monkeypatch):
+    """A host input registered over fewer rows than a view uploads (the
+    bench pins each rank's rows; a fused chain's view is KL rows deeper) must
+    go through a fresh copy: a DMA straddling a registration edge is invalid,
+    and np.ascontiguousarray of a contiguous slice would alias the input."""
+    lib = fake(1)
+    seen = []
+    orig = type(lib).cq_copy_box_h2d
+
+    def spy(self, d, s, eb, dst, host, halloc, box):
+        seen.append(getattr(host, "value", host))
+        return orig(self, d, s, eb, dst, host, halloc, box)
+    monkeypatch.setattr(type(lib), "cq_copy_box_h2d", spy)
+    monkeypatch.setattr(E, "_pin_state", lambda start, end: "partial")
+    h, w = 64, 32
+    u0 = np.random.default_rng(1).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=2, kind="float32", u0=u0, up0=u0)
+    res = E.run(cq.generate_commands(prog.graph(), 1), placement=E.Placement(1, 0, (0,)))
+    base, end = u0.ctypes.data, u0.ctypes.data + u0.nbytes
+    assert seen and all(not (base <= p < end) for p in seen)
+    from oracle import native as onat
+    u, up = onat.wave_run(u0, u0, 2, 0.25)
+    assert dsl.same_bits(res.buffers["u"], u)
