@@ -431,7 +431,7 @@ class Session:
         need = {}
         for (node, buf), view in self.views.items():
             if node == 0 and self.buffers[buf].init.kind in ("array", "values"):
-                need.setdefault(buf, []).append(view.box)
+                need.setdefault(buf, []).append(self.seed_box.get((node, buf)) or view.box)
         for c in self.plan.commands:
             if isinstance(c, PushCommand) and not c.deps and self.local(c.dst) \
                     and self.buffers[c.buffer].init.kind in ("array", "values"):
@@ -519,6 +519,9 @@ class Session:
                     continue  # gathered straight from the host array
                 for h in holders:
                     touch.setdefault((h, name), []).append(reg.bounding_box())
+        # what node 0 uploads: everything it touches in the plan itself (the
+        # deeper fused halo rows are filled by the first exchange)
+        self.seed_box = {k: _bbox_union(v) for k, v in touch.items()}
         fused = set()
         for ch in self.chains:
             # fused blocks read a KL-deep halo and write out of place
@@ -587,7 +590,8 @@ class Session:
         for (node, buf), view in self.views.items():
             if node != 0 or not self.buffers[buf].init.is_initialized:
                 continue
-            self.materialize(0, buf, Region.from_box(view.box), N.STREAM_COMM)
+            box = self.seed_box.get((node, buf)) or view.box
+            self.materialize(0, buf, Region.from_box(box), N.STREAM_COMM)
 
     # ---- transfers -------------------------------------------------------
     def flush_group(self, group):
