@@ -99,7 +99,7 @@ _SIGS = {
     "cq_saxpy": (i32, [i32, i32, i32, ctypes.c_double, i64, vp, vp, vp, i64]),
     "cq_wave5": (i32, [i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqBox), P(CqBox),
                        ctypes.c_double, ctypes.c_double, ctypes.c_double]),
-    "cq_wave5_fused": (i32, [i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqView), i64, i64, i64, i64,
+    "cq_wave5_fused": (i32, [i32, i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqView), i64, i64, i64, i64,
                              P(CqBox), ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     "cq_expr_eval": (i32, [i32, i32, P(CqExpr)]),
     "cq_error_flag": (i32, [i32, P(i32), P(i64), i32]),

@@ -546,10 +546,13 @@ __global__ void nbody_drift_kernel(const float4* p_in, const float4* __restrict_
 // static).  Global borders clamp exactly like the DSL's ReadView (the border
 // cell reads itself).  Rows outside [in_lo, in_hi) are not read; the caller
 // keeps [out_lo, out_hi) inside the trapezoid they determine.
-template <int V> struct FVec;
-template <> struct FVec<2> { typedef float2 T; };
-template <> struct FVec<4> { typedef float4 T; };
+template <typename T, int V> struct FVec;
+template <> struct FVec<float, 2> { typedef float2 T; };
+template <> struct FVec<float, 4> { typedef float4 T; };
+template <> struct FVec<double, 2> { typedef double2 T; };
 
+__device__ __forceinline__ double first_of(double2 v) { return v.x; }
+__device__ __forceinline__ double last_of(double2 v) { return v.y; }
 __device__ __forceinline__ float first_of(float2 v) { return v.x; }
 __device__ __forceinline__ float last_of(float2 v) { return v.y; }
 __device__ __forceinline__ float first_of(float4 v) { return v.x; }
@@ -574,6 +577,16 @@ __device__ __forceinline__ float2 wave_vec(float2 m, float2 n, float2 s, float2 
   float2 r;
   unpack2(o, r.x, r.y);
   return r;
+}
+
+// float64 (the reference's own element kind): scalar DADD/DMUL, which ptxas
+// does not contract
+__device__ __forceinline__ double2 wave_vec(double2 m, double2 n, double2 s, double2 p, double wv, double ev,
+                                            double c) {
+  double2 o;
+  o.x = wave_cell<double>(m.x, p.x, n.x, s.x, wv, m.y, c, 2.0, 4.0);
+  o.y = wave_cell<double>(m.y, p.y, n.y, s.y, m.x, ev, c, 2.0, 4.0);
+  return o;
 }
 
 __device__ __forceinline__ float4 wave_vec(float4 m, float4 n, float4 s, float4 p, float wv, float ev, float c) {
@@ -606,12 +619,11 @@ __device__ __forceinline__ void cp_async_wait() {
 // (cp.async, one commit group per row, each lane fetches and later reads
 // back only its own V columns), so D rows of both inputs are in flight per
 // warp without holding them in registers.
-template <int KL, int V, int D, int RB>
+template <typename T, int KL, int V, int D, int RB>
 __global__ void __launch_bounds__(256, 2)
     wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last, cq_view_t out_prev, int64_t in_lo,
-                       int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, float c, float k2,
-                       float k4) {
-  typedef typename FVec<V>::T Vec;
+                       int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c, T k2, T k4) {
+  typedef typename FVec<T, V>::T Vec;
   static_assert(KL >= 2 && KL % V == 0, "strip offsets must stay vector aligned");
   static_assert(D % 3 == 0, "prefetch ring must be a multiple of the window");
   constexpr int SW = 32 * V - 2 * KL;
@@ -633,10 +645,10 @@ __global__ void __launch_bounds__(256, 2)
   // readable.  Border strips / segments take the checked path.
   const bool interior = c0 > 0 && c0 + 32 * V < W && rb - KL > 0 && re < H && rb >= in_lo && re <= in_hi;
   const int64_t us = u.stride[1], ps = upr.stride[1];
-  const float* ub = (const float*)u.ptr + (colok ? col : 0) - u.alloc.lo[2] + (rb - u.alloc.lo[1]) * us;
-  const float* pb = (const float*)upr.ptr + (colok ? col : 0) - upr.alloc.lo[2] + (rb - upr.alloc.lo[1]) * ps;
-  float* sl = (float*)out_last.ptr + (col - out_last.alloc.lo[2]) + (r0 - out_last.alloc.lo[1]) * out_last.stride[1];
-  float* sp = (float*)out_prev.ptr + (col - out_prev.alloc.lo[2]) + (r0 - out_prev.alloc.lo[1]) * out_prev.stride[1];
+  const T* ub = (const T*)u.ptr + (colok ? col : 0) - u.alloc.lo[2] + (rb - u.alloc.lo[1]) * us;
+  const T* pb = (const T*)upr.ptr + (colok ? col : 0) - upr.alloc.lo[2] + (rb - upr.alloc.lo[1]) * ps;
+  T* sl = (T*)out_last.ptr + (col - out_last.alloc.lo[2]) + (r0 - out_last.alloc.lo[1]) * out_last.stride[1];
+  T* sp = (T*)out_prev.ptr + (col - out_prev.alloc.lo[2]) + (r0 - out_prev.alloc.lo[1]) * out_prev.stride[1];
   const int64_t ls = out_last.stride[1], pstr = out_prev.stride[1];
 
   auto march = [&](auto edge_tag) {
@@ -676,8 +688,8 @@ __global__ void __launch_bounds__(256, 2)
             const int64_t rho = ri - j;
             const Vec mid = L[j - 1][sm];
             Vec nn = L[j - 1][so], ss = L[j - 1][s];
-            float wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
-            float ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
+            T wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
+            T ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
             if (EDGE) {
               if (rho == 0) nn = mid;
               if (rho == H - 1) ss = mid;
@@ -705,15 +717,15 @@ __global__ void __launch_bounds__(256, 2)
   cp_async_wait<0>();
 }
 
-template <int KL, int V, int D, int RB>
+template <typename T, int KL, int V, int D, int RB>
 static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& upr, const cq_view_t& ol,
                         const cq_view_t& op, int64_t in_lo, int64_t in_hi, int64_t out_lo, int64_t out_hi,
-                        int64_t H, int64_t W, float c, float k2, float k4) {
+                        int64_t H, int64_t W, T c, T k2, T k4) {
   constexpr int sw = 32 * V - 2 * KL;
   const int64_t strips = (W + sw - 1) / sw;
   dim3 grid((unsigned)((strips + 7) / 8), (unsigned)((out_hi - out_lo + RB - 1) / RB));
-  auto kern = wave5_fused_kernel<KL, V, D, RB>;
-  const int smem = 8 * D * 2 * 32 * V * (int)sizeof(float);
+  auto kern = wave5_fused_kernel<T, KL, V, D, RB>;
+  const int smem = 8 * D * 2 * 32 * V * (int)sizeof(T);
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, 256, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4);
   return CQ_OK;
@@ -812,13 +824,14 @@ int cq_wave5(int device, int stream, int kind, const cq_view_t* u, const cq_view
   return CQ_OK;
 }
 
-int cq_wave5_fused(int device, int stream, int levels, const cq_view_t* u, const cq_view_t* upr,
+int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t* u, const cq_view_t* upr,
                    const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
                    int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4) {
   CQ_GET_STREAM(device, stream);
   if (out_hi <= out_lo) return CQ_OK;
   const int64_t H = extent->hi[1], W = extent->hi[2];
   CQ_REQUIRE(levels == 4 || levels == 8, "cq_wave5_fused: levels must be 4 or 8 (got %d)", levels);
+  CQ_REQUIRE(kind == CQ_F32 || kind == CQ_F64, "cq_wave5_fused: float kinds only");
   CQ_REQUIRE(W % 4 == 0, "cq_wave5_fused: row length must be a multiple of 4");
   CQ_REQUIRE(k2 == 2.0 && k4 == 4.0, "cq_wave5_fused: the body's constants must be k2 = 2, k4 = 4");
   for (const cq_view_t* v : {u, upr, out_last, out_prev}) {
@@ -844,11 +857,20 @@ int cq_wave5_fused(int device, int stream, int levels, const cq_view_t* u, const
   }();
   const int cfg = cfg_env ? cfg_env : (levels == 8 ? 2 * 10000 + 12 * 1000 + 128 : 4 * 10000 + 6 * 1000 + 128);
   int status;
+  if (kind == CQ_F64) {
+    // two doubles per lane (16-byte rows), 56 valid columns per warp strip
+    CQ_REQUIRE(levels == 4, "cq_wave5_fused: float64 runs 4 steps per pass");
+    status = launch_fused<double, 4, 2, 6, 128>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H,
+                                                W, c, k2, k4);
+    if (status != CQ_OK) return status;
+    CQ_CHECK_LAUNCH();
+    return CQ_OK;
+  }
   switch (cfg * 10 + levels) {
 #define CQ_FUSED_CASE(VV, DD, RBB, KL)                                                               \
   case (VV * 10000 + DD * 1000 + RBB) * 10 + KL:                                                   \
-    status = launch_fused<KL, VV, DD, RBB>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H, W, \
-                                           (float)c, (float)k2, (float)k4);                       \
+    status = launch_fused<float, KL, VV, DD, RBB>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, \
+                                                  H, W, (float)c, (float)k2, (float)k4);                       \
     break;
     CQ_FUSED_CASE(4, 6, 128, 4) CQ_FUSED_CASE(4, 6, 128, 8)
     CQ_FUSED_CASE(4, 6, 256, 4) CQ_FUSED_CASE(4, 6, 256, 8)

@@ -784,7 +784,8 @@ class Session:
                 acc = [(ua, rin, False), (pb, rin, False), (oa, rout, True), (ob, rout, True)]
 
                 def go(stream=stream, rng=rng):
-                    N.call("cq_wave5_fused", dev, stream, kl, ctypes.byref(ua.c), ctypes.byref(pb.c),
+                    N.call("cq_wave5_fused", dev, stream, N.KIND_CODE[b.element_kind], kl, ctypes.byref(ua.c),
+                           ctypes.byref(pb.c),
                            ctypes.byref(oa.c), ctypes.byref(ob.c), rng[0], rng[1], rng[2], rng[3],
                            ctypes.byref(ext), ctypes.c_double(ch.c), ctypes.c_double(ch.k2),
                            ctypes.c_double(ch.k4))

@@ -1,7 +1,7 @@
 """Temporal blocking of wave ping-pong chains (an executor optimisation).
 
 A run of consecutive tasks that all bind to the ``wave5`` fast path and
-ping-pong between the same two float32 buffers (task i+1 reads as ``u`` what
+ping-pong between the same two float32 (or float64) buffers (task i+1 reads as ``u`` what
 task i wrote and writes into what task i read as ``u`` -- the shape
 ``workloads.wave_task`` builds) is executed KL steps per HBM
 pass by ``cq_wave5_fused`` instead of one ``cq_wave5`` launch per step:
@@ -121,8 +121,11 @@ def _wave_info(task, buffers):
     if obuf != pbuf or ubuf == pbuf:
         return None
     bu, bp = buffers[ubuf], buffers[pbuf]
-    if bu.element_kind != "float32" or bp.element_kind != "float32" or bu.extent != bp.extent:
+    if bu.element_kind not in ("float32", "float64") or bp.element_kind != bu.element_kind \
+            or bu.extent != bp.extent:
         return None
+    if b.args["k2"] != 2.0 or b.args["k4"] != 4.0:
+        return None   # the fused kernel forms 2u and 4u as exact sums
     ext = bu.extent
     if ext.mins != (0, 0) or task.global_range != ext:
         return None
@@ -167,14 +170,14 @@ def _halo_pushes_ok(pushes, ubuf, rows, W):
     return True
 
 
-def _blocks(tids):
-    """KL=4 blocks, an even number of them (one KL=8 block fixes the parity);
-    leftover tasks run plain."""
+def _blocks(tids, kind="float32"):
+    """KL=4 blocks, an even number of them (float32: one KL=8 block fixes the
+    parity; float64: four plain steps do); leftover tasks run plain."""
     q, r = divmod(len(tids), KL_BASE)
     if q % 2 == 1:
         if q == 1:
             return [], tuple(tids)
-        sizes = [KL_BASE] * (q - 2) + [KL_PARITY]
+        sizes = [KL_BASE] * (q - 2) + [KL_PARITY] if kind == "float32" else [KL_BASE] * (q - 1)
     else:
         sizes = [KL_BASE] * q
     blocks, i = [], 0
@@ -200,7 +203,7 @@ def find_chains(plan, steps):
         info, rows, tids = cur
         if len(tids) < MIN_CHAIN:
             return
-        blocks, plain = _blocks(tids)
+        blocks, plain = _blocks(tids, buffers[info[0]].element_kind)
         if not blocks:
             return
         u0, p0, c, k2, k4, H, W = info

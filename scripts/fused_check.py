@@ -36,7 +36,7 @@ def plain(a, b, h, w, steps, rows=None, C=C):
 def fused(a, b, h, w, kl, in_rows, out_rows, C=C):
     ol, op = torch.full_like(a, float("nan")), torch.full_like(a, float("nan"))
     ext = N.box3((0, 0), (h, w))
-    N.call("cq_wave5_fused", 0, 0, kl, ctypes.byref(view(a, h, w)), ctypes.byref(view(b, h, w)),
+    N.call("cq_wave5_fused", 0, 0, N.CQ_F32, kl, ctypes.byref(view(a, h, w)), ctypes.byref(view(b, h, w)),
            ctypes.byref(view(ol, h, w)), ctypes.byref(view(op, h, w)), in_rows[0], in_rows[1],
            out_rows[0], out_rows[1], ctypes.byref(ext), C, K2, K4)
     return ol, op
@@ -125,7 +125,7 @@ for kl in (4, 8):
         ev[0].record()
         src, dst = (va, vb), (va2, vb2)
         for _ in range(steps // kl):
-            N.call("cq_wave5_fused", 0, 0, kl, ctypes.byref(src[0]), ctypes.byref(src[1]), ctypes.byref(dst[0]),
+            N.call("cq_wave5_fused", 0, 0, N.CQ_F32, kl, ctypes.byref(src[0]), ctypes.byref(src[1]), ctypes.byref(dst[0]),
                    ctypes.byref(dst[1]), 0, h, 0, h, ctypes.byref(ext), C, K2, K4)
             src, dst = dst, src
         ev[1].record()

@@ -13,7 +13,7 @@ def view(x):
 vs = [view(x) for x in t]
 ext = N.box3((0, 0), (h, w))
 for i in range(3):
-    N.call("cq_wave5_fused", 0, 0, kl, ctypes.byref(vs[0]), ctypes.byref(vs[1]), ctypes.byref(vs[2]),
+    N.call("cq_wave5_fused", 0, 0, N.CQ_F32, kl, ctypes.byref(vs[0]), ctypes.byref(vs[1]), ctypes.byref(vs[2]),
            ctypes.byref(vs[3]), 0, h, 0, h, ctypes.byref(ext), 0.25, 2.0, 4.0)
 N.call("cq_stream_synchronize", 0, 0)
 print("ok")

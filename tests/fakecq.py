@@ -269,14 +269,14 @@ class FakeLib:
         self.launches.append("wave5")
         return 0
 
-    def cq_wave5_fused(self, d, s, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi, ext, c, k2,
-                       k4):
+    def cq_wave5_fused(self, d, s, kind, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi, ext, c,
+                       k2, k4):
         """KL ping-pong steps on rows [in_lo, in_hi) (edge rows replicate,
         which is exact at the true borders and only spoils rows outside the
         trapezoid), then rows [out_lo, out_hi) of the last two levels."""
         u, upr, ol, op, e = (_obj(x) for x in (u, upr, out_last, out_prev, ext))
         in_lo, in_hi, out_lo, out_hi, levels = (_val(x) for x in (in_lo, in_hi, out_lo, out_hi, levels))
-        dt = np.float32
+        dt = _DT[_val(kind)]
         W = e.hi[2]
         box = N.box3((in_lo, 0), (in_hi, W))
         cur = self._view(u, dt, box)[0].copy()

@@ -324,3 +324,22 @@ def test_partially_pinned_input_is_bounced_through_a_copy(fake, monkeypatch):
     from oracle import native as onat
     u, up = onat.wave_run(u0, u0, 2, 0.25)
     assert dsl.same_bits(res.buffers["u"], u)
+
+
+def test_fused_wave_chain_float64(fake):
+    """float64 (the reference's own kind) chains fuse too; an odd block count
+    is fixed by plain steps (no KL=8 block)."""
+    from oracle import native as onat
+    fake(1)
+    h, w, steps = 160, 48, 22
+    u0 = np.random.default_rng(31).uniform(0, 1, (h, w))
+    prog = W.wave_program(h, w, steps=steps, kind="float64", c=0.3, u0=u0, up0=u0)
+    s = E.Session(cq.generate_commands(prog.graph(), 2), E.Placement(1, 0, (0,)))
+    ch = s.chains[0]
+    assert [b.kl for b in ch.blocks] == [4] * 4 and len(ch.plain) == 6
+    s.execute(upload=True)
+    s.synchronize()
+    res = s.results()
+    s.close()
+    u, up = onat.wave_run(u0, u0, steps, 0.3)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)

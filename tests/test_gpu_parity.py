@@ -150,6 +150,26 @@ def test_fused_wave_chain_bit_exact_vs_oracle(nodes, steps, c):
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
 
 
+@pytest.mark.parametrize("nodes,steps", [(1, 22), (3, 16)])
+def test_fused_wave_chain_float64_bit_exact(nodes, steps):
+    """The float64 fused kernel (two doubles per lane, scalar DADD/DMUL) is
+    bit-identical to the float64 per-step oracle."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    h, w = 517, 384
+    u0 = np.random.default_rng(41).uniform(0, 1, (h, w))
+    up0 = np.random.default_rng(42).uniform(0, 1, (h, w))
+    u0[:, :5] *= 1e-300
+    prog = W.wave_program(h, w, steps=steps, kind="float64", c=0.3, u0=u0, up0=up0)
+    s = Session(cq.generate_commands(prog.graph(), nodes), Placement(1, 0, (0,)))
+    assert s.chains
+    s.execute(upload=True)
+    s.synchronize()
+    res = s.results()
+    s.close()
+    u, up = onat.wave_run(u0, up0, steps, 0.3)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
 def test_fused_wave_graph_replay_continues_the_simulation():
     """A captured fused execution replayed twice == two more plain fused
     executions == the 3x-longer simulation (the KL-row exchange makes a
