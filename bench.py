@@ -515,7 +515,9 @@ def bench_kernels(args, dist, placement, peaks):
         plan = cq.generate_commands(g, world)
         sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=3, warm=1)
         fk = "wave5_fused4" if "wave5_fused4" in kinds else "wave5"
-        kb = 16 if fk != "wave5" else esize   # algorithmic bytes per cell per launch
+        # algorithmic bytes per cell per launch: fused = read X(t), X(t-1) and
+        # write two levels (4 elements), one-step = 3 elements
+        kb = esize // 3 * 4 if fk != "wave5" else esize
         wk = kinds.get(fk, [0, 1.0, 1])
         value = esize * rows * args.size * steps * 3 / (ms / 1e3) / 1e9
         out[label] = {"value": value, "unit": "GB/s", "scaling": "weak" if "weak" in label else "strong",
