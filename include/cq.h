@@ -14,7 +14,8 @@
  *   - plain pointers and sizes only: device pointers come from cq_malloc,
  *     host pointers are caller-owned (pin with cq_host_register);
  *   - all work is asynchronous on the stream named by (device, stream) with
- *     stream in {CQ_STREAM_COMPUTE, CQ_STREAM_BOUNDARY, CQ_STREAM_COMM};
+ *     stream in {CQ_STREAM_COMPUTE, CQ_STREAM_BOUNDARY, CQ_STREAM_COMM,
+ *     CQ_STREAM_LANE0 .. CQ_STREAM_LANE0 + CQ_NUM_LANES - 1};
  *   - element kinds: CQ_F64 / CQ_F32 / CQ_I64.
  *   - one process may own several devices; multi-process runs use NCCL
  *     (cq_nccl_*), one rank per GPU.
@@ -41,7 +42,16 @@ enum {
 };
 
 enum { CQ_F64 = 0, CQ_F32 = 1, CQ_I64 = 2 };
-enum { CQ_STREAM_COMPUTE = 0, CQ_STREAM_BOUNDARY = 1, CQ_STREAM_COMM = 2, CQ_NUM_STREAMS = 3 };
+/* Lanes: extra default-priority compute streams, so the executes of several
+ * plan nodes sharing one device (independent allocations) run concurrently. */
+enum {
+  CQ_STREAM_COMPUTE = 0,
+  CQ_STREAM_BOUNDARY = 1,
+  CQ_STREAM_COMM = 2,
+  CQ_STREAM_LANE0 = 3,
+  CQ_NUM_LANES = 4,
+  CQ_NUM_STREAMS = 7
+};
 
 #define CQ_MAX_DIMS 3
 

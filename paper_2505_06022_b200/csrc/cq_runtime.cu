@@ -49,6 +49,8 @@ int ensure_device(int device) {
   CQ_CHECK_CUDA(cudaStreamCreateWithPriority(&d.streams[CQ_STREAM_COMPUTE], cudaStreamNonBlocking, lo));
   CQ_CHECK_CUDA(cudaStreamCreateWithPriority(&d.streams[CQ_STREAM_BOUNDARY], cudaStreamNonBlocking, hi));
   CQ_CHECK_CUDA(cudaStreamCreateWithPriority(&d.streams[CQ_STREAM_COMM], cudaStreamNonBlocking, hi));
+  for (int l = 0; l < CQ_NUM_LANES; ++l)
+    CQ_CHECK_CUDA(cudaStreamCreateWithPriority(&d.streams[CQ_STREAM_LANE0 + l], cudaStreamNonBlocking, lo));
   CQ_CHECK_CUDA(cudaMalloc(&d.error_flag, 8 * sizeof(int)));
   // error key all-ones == "no error" (atomicMin records the first failure)
   CQ_CHECK_CUDA(cudaMemset(d.error_flag, 0xff, 2 * sizeof(int)));
@@ -478,14 +480,12 @@ int cq_device_synchronize(int device) {
 // compute stream waits on before the capture ends.
 int cq_graph_begin(int device) {
   CQ_STREAM(device, CQ_STREAM_COMPUTE);
-  cudaStream_t b = stream_of(device, CQ_STREAM_BOUNDARY), c = stream_of(device, CQ_STREAM_COMM);
   CQ_CHECK_CUDA(cudaSetDevice(device));
   CQ_CHECK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
   cudaEvent_t fork;
   CQ_CHECK_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
   CQ_CHECK_CUDA(cudaEventRecord(fork, st));
-  CQ_CHECK_CUDA(cudaStreamWaitEvent(b, fork, 0));
-  CQ_CHECK_CUDA(cudaStreamWaitEvent(c, fork, 0));
+  for (int s = 1; s < CQ_NUM_STREAMS; ++s) CQ_CHECK_CUDA(cudaStreamWaitEvent(stream_of(device, s), fork, 0));
   CQ_CHECK_CUDA(cudaEventDestroy(fork));
   return CQ_OK;
 }
@@ -493,7 +493,7 @@ int cq_graph_begin(int device) {
 int cq_graph_end(int device, uint64_t* graph) {
   CQ_STREAM(device, CQ_STREAM_COMPUTE);
   CQ_CHECK_CUDA(cudaSetDevice(device));
-  for (int s : {CQ_STREAM_BOUNDARY, CQ_STREAM_COMM}) {
+  for (int s = 1; s < CQ_NUM_STREAMS; ++s) {
     cudaEvent_t join;
     CQ_CHECK_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
     CQ_CHECK_CUDA(cudaEventRecord(join, stream_of(device, s)));

@@ -699,12 +699,28 @@ class Session:
             self.trace_marks.append((push, node, self.dev(node), start, stop))
 
     # ---- executes --------------------------------------------------------
+    def lane(self, node):
+        """Compute stream of a node: with several local nodes on one device
+        (independent allocations) each gets its own lane, so their executes
+        run concurrently; otherwise the compute stream."""
+        lanes = getattr(self, "_lanes", None)
+        if lanes is None:
+            lanes = self._lanes = {}
+            by_dev = {}
+            for n in self.local_nodes:
+                by_dev.setdefault(self.dev(n), []).append(n)
+            for nodes in by_dev.values():
+                for i, n in enumerate(sorted(nodes)):
+                    lanes[n] = N.STREAM_COMPUTE if i == 0 else N.STREAM_LANE0 + (i - 1) % N.NUM_LANES
+        return lanes.get(node, N.STREAM_COMPUTE)
+
     def exec_command(self, cmd: ExecuteCommand, awaited):
         task = self.plan.graph.task(cmd.task_id)
         binding = self.bindings.get(task.id)
         if binding is None:
             binding = self.bindings[task.id] = bind_task(task, self.buffers)
         node, dev = cmd.node, self.dev(cmd.node)
+        lane = self.lane(node)
         rviews = {}
         for a in task.accessors:
             if a.mode is AccessMode.READ:
@@ -722,9 +738,9 @@ class Session:
 
             def go(src=src, snap=snap, reg=reg):
                 for box in reg.boxes:
-                    N.call("cq_copy_box", dev, N.STREAM_COMPUTE, src.itemsize, ctypes.byref(snap.c), dev,
+                    N.call("cq_copy_box", dev, lane, src.itemsize, ctypes.byref(snap.c), dev,
                            ctypes.byref(src.c), dev, ctypes.byref(_cbox(box)))
-            self.issue(dev, N.STREAM_COMPUTE, [(node, buf, reg, False)], go)
+            self.issue(dev, lane, [(node, buf, reg, False)], go)
             rviews[name] = snap
 
         pieces = self.split(task, cmd, awaited)
@@ -732,7 +748,7 @@ class Session:
         for box, dependent in pieces:
             # only a split chunk sends its halo-dependent rows to the
             # high-priority stream; an unsplit chunk stays on the compute one
-            stream = N.STREAM_BOUNDARY if dependent and len(pieces) > 1 else N.STREAM_COMPUTE
+            stream = N.STREAM_BOUNDARY if dependent and len(pieces) > 1 else lane
             acc = []
             for a in task.accessors:
                 if a.mode is AccessMode.READ:
@@ -774,7 +790,7 @@ class Session:
             oa, ob = self.alt[(node, ch.a)], self.alt[(node, ch.b)]
             marks = []
             interior, edge_t, edge_b = fusion.node_ranges(ch, node, kl)
-            for rng, stream in ((interior, N.STREAM_COMPUTE), (edge_t, N.STREAM_BOUNDARY),
+            for rng, stream in ((interior, self.lane(node)), (edge_t, N.STREAM_BOUNDARY),
                                 (edge_b, N.STREAM_BOUNDARY)):
                 if rng is None or rng[3] <= rng[2]:
                     continue
@@ -1055,7 +1071,7 @@ class Session:
                 ev = self.event(d, timing=True)
                 N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
                 self._t0[d] = ev
-                for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
+                for s in N.SIDE_STREAMS:
                     N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
             self.t0 = dict(self._t0)
         self.uploading = upload
@@ -1137,13 +1153,13 @@ class Session:
         per device on the compute stream; returns {device: event}."""
         out = {}
         for d in self.devices:
-            for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
+            for s in N.SIDE_STREAMS:
                 ev = self.event(d)
                 N.call("cq_event_record", ctypes.c_uint64(ev), d, s)
                 N.call("cq_stream_wait_event", d, N.STREAM_COMPUTE, ctypes.c_uint64(ev))
             ev = self.event(d, timing=True)
             N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
-            for s in (N.STREAM_BOUNDARY, N.STREAM_COMM):
+            for s in N.SIDE_STREAMS:
                 N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
             out[d] = ev
         return out
@@ -1156,7 +1172,7 @@ class Session:
 
     def synchronize(self):
         for d in self.devices:
-            for s in (N.STREAM_COMPUTE, N.STREAM_BOUNDARY, N.STREAM_COMM):
+            for s in N.ALL_STREAMS:
                 N.call("cq_stream_synchronize", d, s)
         self.bounce.clear()
         self.check_errors()
