@@ -13,7 +13,7 @@ Buffer/Task/TaskGraph -> generate_commands -> B200 executor.
 * e2e       -- the public call ``run(plan)`` with pinned host input arrays
                (H2D inside the timed region) and the result read back to host.
 * roofline  -- the dominant kernel: the temporally blocked wave pass
-               (cq_wave5_fused, 4 time steps per HBM pass: 16 algorithmic
+               (cq_wave5_fused, 8 time steps per HBM pass: 16 algorithmic
                bytes per cell per launch) -- or the one-step kernel (12 B/cell)
                with CQ_WAVE_FUSE=0 -- over its CUDA-event launch time, against
                MEASURED_PEAKS.json hbm_gbs.  ``value`` keeps the SURVEY unit
@@ -223,8 +223,11 @@ def bench_wave(args, dist, placement, peaks):
     # the dominant kernel: the temporally blocked KL=4 pass when the chain is
     # fused (16 algorithmic B/cell per launch: read X(t), X(t-1), write
     # X(t+4), X(t+3)), else the one-step kernel (12 B/cell)
-    kinds_seen = {x[0] for x in sess.launch_log}
-    dom_kind = "wave5_fused4" if "wave5_fused4" in kinds_seen else "wave5"
+    totals = {}
+    for x in sess.launch_log:
+        if x[0].startswith("wave5"):
+            totals[x[0]] = totals.get(x[0], 0) + x[1]
+    dom_kind = max(totals, key=totals.get)   # most cells: wave5_fused8 / _fused4 / wave5
     bpc = 16 if dom_kind != "wave5" else 12
     wave_launches = [x for x in sess.launch_log if x[0] == dom_kind]
     launches_per_replay = len(sess.launch_log)
@@ -312,7 +315,7 @@ def bench_wave(args, dist, placement, peaks):
     finite = bool(np.isfinite(field).all())
 
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "wave5_fused_traffic.json" if bpc == 16 else "wave5_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", f"{dom_kind}_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             t = json.load(fh)
@@ -325,12 +328,18 @@ def bench_wave(args, dist, placement, peaks):
                 "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks[0]["hbm_gbs"], "traffic": traffic,
-                     "kernel": ("wave5_fused_kernel<4,4,6,128> (4 time steps per pass)" if bpc == 16
-                                else "wave5_rows_kernel<float,32>"),
+                     "kernel": {"wave5_fused8": "wave5_fused_kernel<float,8,4,6,256> (8 time steps per pass)",
+                                "wave5_fused4": "wave5_fused_kernel<float,4,4,6,128> (4 time steps per pass)"}.get(
+                                    dom_kind, "wave5_rows_kernel<float,32>"),
                      "bytes_per_cell": bpc,
                      "cells_per_launch": dom_launch[1], "launches": len(dominant),
                      "bytes_per_launch": bpc * dom_launch[1],
                      "peak_source": peaks[1] + " hbm_gbs (torch copy)",
+                     "note": ("8 time steps per HBM pass: twice the arithmetic per byte of the 4-step pass; "
+                              "the kernel is FP32-pipe / issue limited (ncu: FMA pipe 63% active, issue slots "
+                              "64% busy; profiles/r01/wave5_fused8_ncu_full_summary.txt), so its HBM fraction is "
+                              "below 1 while the step is 1.3x faster than 4-step passes at 0.85 of HBM")
+                             if dom_kind == "wave5_fused8" else None,
                      "launch_timing": timing_source},
         "clocks": clk,
         "gpu_launches": gpu_launches,
@@ -514,7 +523,7 @@ def bench_kernels(args, dist, placement, peaks):
         del z
         plan = cq.generate_commands(g, world)
         sess, ms, kinds, _ = _timed_session(plan, placement, dist, reps=3, warm=1)
-        fk = "wave5_fused4" if "wave5_fused4" in kinds else "wave5"
+        fk = max((k for k in kinds if k.startswith("wave5")), key=lambda k: kinds[k][0], default="wave5")
         # algorithmic bytes per cell per launch: fused = read X(t), X(t-1) and
         # write two levels (4 elements), one-step = 3 elements
         kb = esize // 3 * 4 if fk != "wave5" else esize

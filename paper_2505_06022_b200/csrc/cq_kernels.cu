@@ -619,8 +619,18 @@ __device__ __forceinline__ void cp_async_wait() {
 // (cp.async, one commit group per row, each lane fetches and later reads
 // back only its own V columns), so D rows of both inputs are in flight per
 // warp without holding them in registers.
+// 8 warps per block; the register-heavy KL = 8, V = 4 variant (~200
+// registers per thread) runs one block per SM -- more warps would cap it at
+// 168 registers (3 warps per SM sub-partition) and spill, which measured
+// slower (profiles/r01/fused_cfg_sweep.log).
+template <int KL, int V>
+struct FusedShape {
+  static constexpr int kWarps = 8;
+  static constexpr int kMinBlocks = (KL == 8 && V == 4) ? 1 : 2;
+};
+
 template <typename T, int KL, int V, int D, int RB>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL, V>::kMinBlocks)
     wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last, cq_view_t out_prev, int64_t in_lo,
                        int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c, T k2, T k4) {
   typedef typename FVec<T, V>::T Vec;
@@ -630,7 +640,7 @@ __global__ void __launch_bounds__(256, 2)
   extern __shared__ __align__(16) uint8_t fused_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   Vec* ring = reinterpret_cast<Vec*>(fused_smem) + (size_t)warp * D * 2 * 32;  // [D][2][32]
-  const int64_t strip = (int64_t)blockIdx.x * 8 + warp;
+  const int64_t strip = (int64_t)blockIdx.x * FusedShape<KL, V>::kWarps + warp;
   const int64_t r0 = out_lo + (int64_t)blockIdx.y * RB;
   if (strip * SW >= W || r0 >= out_hi) return;  // warp-uniform
   const int64_t r1 = min(r0 + (int64_t)RB, out_hi);
@@ -723,11 +733,12 @@ static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& up
                         int64_t H, int64_t W, T c, T k2, T k4) {
   constexpr int sw = 32 * V - 2 * KL;
   const int64_t strips = (W + sw - 1) / sw;
-  dim3 grid((unsigned)((strips + 7) / 8), (unsigned)((out_hi - out_lo + RB - 1) / RB));
+  constexpr int WPB = FusedShape<KL, V>::kWarps;
+  dim3 grid((unsigned)((strips + WPB - 1) / WPB), (unsigned)((out_hi - out_lo + RB - 1) / RB));
   auto kern = wave5_fused_kernel<T, KL, V, D, RB>;
-  const int smem = 8 * D * 2 * 32 * V * (int)sizeof(T);
+  const int smem = WPB * D * 2 * 32 * V * (int)sizeof(T);
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, 256, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4);
+  kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4);
   return CQ_OK;
 }
 
@@ -848,14 +859,14 @@ int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t
              "cq_wave5_fused: rows [%lld, %lld) are not determined by input rows [%lld, %lld)",
              (long long)out_lo, (long long)out_hi, (long long)in_lo, (long long)in_hi);
   // tuning: CQ_WAVE_FUSED_CFG="V,D,RB" (lane width, cp.async ring depth,
-  // rows per warp segment); default 4,6,128 for KL = 4 and 2,12,128 for
-  // KL = 8 (whose 8 register windows fit without spills only at V = 2)
+  // rows per warp segment); default 4,6,128 for KL = 4 (2 blocks / SM) and
+  // 4,6,256 for KL = 8 (1 block / SM: its 8 register windows need ~200 regs)
   static int cfg_env = [] {
     int v = 0, d = 0, rb = 0;
     if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d,%d", &v, &d, &rb);
     return v ? v * 10000 + d * 1000 + rb : 0;
   }();
-  const int cfg = cfg_env ? cfg_env : (levels == 8 ? 2 * 10000 + 12 * 1000 + 128 : 4 * 10000 + 6 * 1000 + 128);
+  const int cfg = cfg_env ? cfg_env : (levels == 8 ? 4 * 10000 + 6 * 1000 + 256 : 4 * 10000 + 6 * 1000 + 128);
   int status;
   if (kind == CQ_F64) {
     // two doubles per lane (16-byte rows), 56 valid columns per warp strip

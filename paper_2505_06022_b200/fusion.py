@@ -20,9 +20,10 @@ What changes against executing the plan command by command: the plan's
 one-row halo pushes of the fused tasks are replaced by one KL-row exchange
 per block; the last task's pushes are still posted after the chain, so every
 halo row the plan's ``final_locations`` lists holds its final version.
-Blocks use KL = 4; an even number of out-of-place blocks (one KL = 8 block
-fixes the parity) keeps the current allocations where a CUDA-graph capture
-found them; leftover steps (< 4) run one step at a time.
+float32 chains run KL = 8 blocks (half the bytes per step of KL = 4) with
+KL = 4 blocks where the parity needs them: an even number of out-of-place
+blocks keeps the current allocations where a CUDA-graph capture found them;
+leftover steps (< 4) run one step at a time.
 
 ``CQ_WAVE_FUSE=0`` disables the transformation.
 """
@@ -171,15 +172,26 @@ def _halo_pushes_ok(pushes, ubuf, rows, W):
 
 
 def _blocks(tids, kind="float32"):
-    """KL=4 blocks, an even number of them (float32: one KL=8 block fixes the
-    parity; float64: four plain steps do); leftover tasks run plain."""
-    q, r = divmod(len(tids), KL_BASE)
-    if q % 2 == 1:
-        if q == 1:
+    """Split a chain into out-of-place blocks with an even count (so the
+    current allocations return to where they started): float32 uses as many
+    KL=8 blocks as the parity allows plus KL=4 blocks (KL=8 moves half the
+    bytes per step); float64 uses KL=4 only, four plain steps fixing an odd
+    count.  Tasks left over (< 4) run plain."""
+    q, _r = divmod(len(tids), KL_BASE)   # quarter blocks
+    if kind == "float32":
+        b = q % 2                          # KL=4 blocks (same parity as q)
+        a = (q - b) // 2                   # KL=8 blocks
+        if (a + b) % 2:
+            a, b = a - 1, b + 2
+        if a < 0:
             return [], tuple(tids)
-        sizes = [KL_BASE] * (q - 2) + [KL_PARITY] if kind == "float32" else [KL_BASE] * (q - 1)
+        sizes = [KL_PARITY] * a + [KL_BASE] * b
     else:
+        if q % 2 == 1:
+            q -= 1
         sizes = [KL_BASE] * q
+    if not sizes:
+        return [], tuple(tids)
     blocks, i = [], 0
     for kl in sizes:
         blocks.append(Block(tuple(tids[i:i + kl]), kl))

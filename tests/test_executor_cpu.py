@@ -148,7 +148,7 @@ def _rank_main(rank, world, port, outdir):
     for nodes in (2, 3):
         prog = W.wave_program(160, 32, steps=14, kind="float32", u0=fu0, up0=fu0)
         sess = E.Session(cq.generate_commands(prog.graph(), nodes), pl)
-        assert [b.kl for b in sess.chains[0].blocks] == [4, 8]
+        assert [b.kl for b in sess.chains[0].blocks] == [8, 4]
         sess.execute(upload=True)
         sess.synchronize()
         res = sess.results()
@@ -284,7 +284,7 @@ def test_fused_chain_disabled_and_graph_replay(fake, monkeypatch):
     s0.close()
     monkeypatch.delenv("CQ_WAVE_FUSE")
     s = E.Session(plan, E.Placement(1, 0, (0,)))
-    assert [b.kl for b in s.chains[0].blocks] == [4, 8]
+    assert [b.kl for b in s.chains[0].blocks] == [8, 4]
     s.execute(upload=True)
     s.synchronize()
     s.recycle()
