@@ -653,7 +653,12 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   const int64_t rb = r0 - KL, re = r1 + KL;  // input rows this warp streams
   // Almost every warp is interior: no border clamping, every input row
   // readable.  Border strips / segments take the checked path.
-  const bool interior = c0 > 0 && c0 + 32 * V < W && rb - KL > 0 && re < H && rb >= in_lo && re <= in_hi;
+  // Decided per block (from blockIdx and parameters only), so the branch is
+  // CTA-uniform and the shuffles inside need no divergence fallback.
+  constexpr int WPB = FusedShape<KL, V>::kWarps;
+  const int64_t bc0 = (int64_t)blockIdx.x * WPB * SW - KL;  // first loaded column of the block
+  const bool interior = bc0 > 0 && bc0 + (WPB - 1) * SW + 32 * V < W && rb - KL > 0 && re < H && rb >= in_lo &&
+                        re <= in_hi;
   const int64_t us = u.stride[1], ps = upr.stride[1];
   const T* ub = (const T*)u.ptr + (colok ? col : 0) - u.alloc.lo[2] + (rb - u.alloc.lo[1]) * us;
   const T* pb = (const T*)upr.ptr + (colok ? col : 0) - upr.alloc.lo[2] + (rb - upr.alloc.lo[1]) * ps;
@@ -681,46 +686,51 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
       if (rb + q < re) fetch(q, rb + q, q);
       cp_async_commit();
     }
-#pragma unroll 1
-    for (int64_t base = rb; base < re; base += D) {
+    // one input row: land it, prefetch row ri + D, advance every level
+    auto row = [&](const int64_t ri, const int sd) {
+      const int s = sd % 3, so = (sd + 1) % 3, sm = (sd + 2) % 3;  // rows ri, ri-2, ri-1
+      cp_async_wait<D - 1>();  // row ri (the oldest group) has landed
+      L[0][s] = ring[(sd * 2 + 0) * 32 + lane];
+      P[s] = ring[(sd * 2 + 1) * 32 + lane];
+      if (ri + D < re) fetch(sd, ri + D, ri + D - rb);
+      cp_async_commit();
 #pragma unroll
-      for (int sd = 0; sd < D; ++sd) {
-        const int64_t ri = base + sd;
-        if (ri < re) {
-          const int s = sd % 3, so = (sd + 1) % 3, sm = (sd + 2) % 3;  // rows ri, ri-2, ri-1
-          cp_async_wait<D - 1>();  // row ri (the oldest group) has landed
-          L[0][s] = ring[(sd * 2 + 0) * 32 + lane];
-          P[s] = ring[(sd * 2 + 1) * 32 + lane];
-          if (ri + D < re) fetch(sd, ri + D, ri + D - rb);
-          cp_async_commit();
-#pragma unroll
-          for (int j = 1; j <= KL; ++j) {
-            const int64_t rho = ri - j;
-            const Vec mid = L[j - 1][sm];
-            Vec nn = L[j - 1][so], ss = L[j - 1][s];
-            T wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
-            T ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
-            if (EDGE) {
-              if (rho == 0) nn = mid;
-              if (rho == H - 1) ss = mid;
-              if (col == 0) wv = first_of(mid);
-              if (col + V == W) ev = last_of(mid);
-            }
-            const Vec pp = (j == 1) ? P[sm] : L[j >= 2 ? j - 2 : 0][so];
-            const Vec o = wave_vec(mid, nn, ss, pp, wv, ev, c);
-            if (j < KL) L[j][s] = o;
-            if (j == KL - 1 && rho >= r0 && rho < r1) {
-              if (keep) __stcs(reinterpret_cast<Vec*>(sp), o);
-              sp += pstr;
-            }
-            if (j == KL && rho >= r0) {
-              if (keep) __stcs(reinterpret_cast<Vec*>(sl), o);
-              sl += ls;
-            }
-          }
+      for (int j = 1; j <= KL; ++j) {
+        const int64_t rho = ri - j;
+        const Vec mid = L[j - 1][sm];
+        Vec nn = L[j - 1][so], ss = L[j - 1][s];
+        T wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
+        T ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
+        if (EDGE) {
+          if (rho == 0) nn = mid;
+          if (rho == H - 1) ss = mid;
+          if (col == 0) wv = first_of(mid);
+          if (col + V == W) ev = last_of(mid);
+        }
+        const Vec pp = (j == 1) ? P[sm] : L[j >= 2 ? j - 2 : 0][so];
+        const Vec o = wave_vec(mid, nn, ss, pp, wv, ev, c);
+        if (j < KL) L[j][s] = o;
+        if (j == KL - 1 && rho >= r0 && rho < r1) {
+          if (keep) __stcs(reinterpret_cast<Vec*>(sp), o);
+          sp += pstr;
+        }
+        if (j == KL && rho >= r0) {
+          if (keep) __stcs(reinterpret_cast<Vec*>(sl), o);
+          sl += ls;
         }
       }
+    };
+    // whole ring turns without a bounds test (the warp stays converged, so
+    // the shuffles need no collective fallback), then the remainder
+    int64_t base = rb;
+#pragma unroll 1
+    for (; base + D <= re; base += D) {
+#pragma unroll
+      for (int sd = 0; sd < D; ++sd) row(base + sd, sd);
     }
+#pragma unroll
+    for (int sd = 0; sd < D; ++sd)
+      if (base + sd < re) row(base + sd, sd);
   };
   if (interior) march(std::false_type{});
   else march(std::true_type{});
