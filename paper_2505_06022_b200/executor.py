@@ -694,9 +694,13 @@ class Session:
 
     # ---- timing marks for the trace ----------------------------------------
     def mark_transfer(self, push, node, events):
-        if self.want_trace and push.id is not None:
-            start, stop = events
-            self.trace_marks.append((push, node, self.dev(node), start, stop))
+        if not self.want_trace:
+            return
+        start, stop = events
+        if push.id is None:   # a fused block's halo transfer (fusion.HaloPush)
+            self._halo_marks.append((push, node, self.dev(node), start, stop))
+            return
+        self.trace_marks.append((push, node, self.dev(node), start, stop))
 
     # ---- executes --------------------------------------------------------
     def lane(self, node):
@@ -768,7 +772,7 @@ class Session:
         if self.want_trace:
             self.trace_marks.append((cmd, node, dev, marks, None))
 
-    def exec_fused(self, ch, block, hostinit):
+    def exec_fused(self, ch, block, hostinit, replaced=()):
         """One temporally blocked wave block (fusion.py): the KL-row halo
         exchange, then per local node the interior launch (compute stream)
         and the neighbour-edge launches (boundary stream, after the
@@ -777,7 +781,16 @@ class Session:
         if hostinit:
             self.flush_group(hostinit)   # upload-time materialisation only
         b = self.buffers[ch.a]
+        self._halo_marks = []
         self.flush_group(fusion.halo_pushes(ch, kl, b.itemsize))
+        if self.want_trace:
+            # the plan's one-row pushes of these tasks travelled inside the
+            # block's halo exchange: trace them with its times
+            for p in replaced:
+                for hp, node, dev, start, stop in self._halo_marks:
+                    if node in (p.src, p.dst) and (hp.src, hp.dst) == (p.src, p.dst):
+                        self.trace_marks.append((p, node, dev, start, stop))
+                        break
         ext = _cbox(b.extent)
         W = ch.W
         if not hasattr(self, "_exec_of"):

@@ -250,7 +250,7 @@ def _task_buffers(task, buffers):
 
 def transform(steps, chains):
     """Replace the steps of every fused block by one ("fused", chain, block,
-    host-init pushes) step; after a chain whose last task is fused, post that
+    host-init pushes, plan pushes the block's exchange replaces) step; after a chain whose last task is fused, post that
     task's plan pushes (so the final halo rows hold their final versions)."""
     if not chains:
         return steps
@@ -269,6 +269,7 @@ def transform(steps, chains):
     out = []
     emitted = set()
     hostinit = {}
+    replaced = {}
     for i, st in enumerate(steps):
         t = owner[i]
         if t is None and st[0] == "group":
@@ -283,9 +284,11 @@ def transform(steps, chains):
         key = (id(ch), bl.tasks[0])
         if st[0] == "group":
             hostinit.setdefault(key, []).extend(p for p in st[1] if not p.deps)
+            posted_later = set(map(id, ch.last_pushes)) if not ch.plain else set()
+            replaced.setdefault(key, []).extend(p for p in st[1] if p.deps and id(p) not in posted_later)
         if key not in emitted:
             emitted.add(key)
-            out.append(("fused", ch, bl, hostinit.setdefault(key, [])))
+            out.append(("fused", ch, bl, hostinit.setdefault(key, []), replaced.setdefault(key, [])))
         if st[0] == "exec" and not ch.plain and t == ch.blocks[-1].tasks[-1] \
                 and _is_last_exec(steps, i, t):
             if ch.last_pushes:

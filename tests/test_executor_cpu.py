@@ -267,8 +267,10 @@ def test_fused_wave_chain_matches_oracle(fake, monkeypatch, steps, nodes, ndev):
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
     if steps >= 8:
         assert "wave5_fused" in lib.launches
-    # one trace event per execute command, fused or not
+    # one trace event per execute and per push command, fused or not
     assert sum(1 for e in trace if e.kind == "execute") == steps * nodes
+    n_push = sum(1 for c in plan.commands if type(c).__name__ == "PushCommand")
+    assert sum(1 for e in trace if e.kind == "push") == n_push
 
 
 def test_fused_chain_disabled_and_graph_replay(fake, monkeypatch):
