@@ -419,6 +419,13 @@ class Session:
         self.bounce = []        # temporaries of bounced host copies (kept until sync)
         for d in self.devices:
             N.call("cq_init_device", d)
+        # several GPUs in one process: box copies between them go peer to
+        # peer over NVLink (they stay correct, staged, without it)
+        for d in self.devices:
+            for e in self.devices:
+                if d != e:
+                    ok = ctypes.c_int32()
+                    N.call("cq_enable_peer", d, e, ctypes.byref(ok))
         kahn_order(plan)  # validates acyclicity before touching devices
         self.alt = {}
         self.chains = fusion.find_chains(plan, self._raw_schedule())
