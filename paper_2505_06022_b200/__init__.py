@@ -64,7 +64,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # The executor pulls in the ctypes binding lazily so that planning-only
     # users (and the CPU test suite) never need the native library.
-    if name in ("run", "RunResult", "TraceEvent", "LinkModel", "trace_to_chrome"):
+    if name in ("run", "run_batch", "RunResult", "TraceEvent", "LinkModel", "trace_to_chrome"):
         from . import executor
         return getattr(executor, name)
     raise AttributeError(name)

@@ -967,6 +967,8 @@ int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const flo
     NB_LAUNCH(1)
     NB_LAUNCH(2)
     NB_LAUNCH(3)
+    NB_LAUNCH(6)
+    NB_LAUNCH(8)
     default:
     NB_LAUNCH(4)
 #undef NB_LAUNCH

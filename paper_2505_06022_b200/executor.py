@@ -389,9 +389,14 @@ class Session:
 
     ``run()`` is one upload + execute + gather; benchmarks use the pieces."""
 
-    def __init__(self, plan: Plan, placement: Optional[Placement] = None, trace: bool = True):
+    def __init__(self, plan: Plan, placement: Optional[Placement] = None, trace: bool = True,
+                 copy_streams=None):
         placement = placement or local_placement()
         self.plan = plan
+        # streams of the host uploads / read-backs (default: the comm stream);
+        # run_batch gives its two sessions their own, so one session's
+        # read-back, the other's upload and the kernels overlap
+        self.h2d_stream, self.d2h_stream = copy_streams or (N.STREAM_COMM, N.STREAM_COMM)
         self.pl = placement
         self.want_trace = trace
         self.buffers = plan.graph.buffers
@@ -412,6 +417,7 @@ class Session:
         self.graph_log = []     # launch_log of a timed capture: its events re-record per replay
         self.graph_events = []
         self.host_init = {}
+        self._overridden = set()
         self._sched = None
         self.t0 = None
         self._t0 = {}
@@ -598,7 +604,7 @@ class Session:
             if node != 0 or not self.buffers[buf].init.is_initialized:
                 continue
             box = self.seed_box.get((node, buf)) or view.box
-            self.materialize(0, buf, Region.from_box(box), N.STREAM_COMM)
+            self.materialize(0, buf, Region.from_box(box), self.h2d_stream)
 
     # ---- transfers -------------------------------------------------------
     def flush_group(self, group):
@@ -611,7 +617,7 @@ class Session:
             if not push.deps:
                 # host-initialised data: the destination materialises it
                 if dst_l and self.uploading:
-                    t = self.materialize(push.dst, push.buffer, push.region, N.STREAM_COMM)
+                    t = self.materialize(push.dst, push.buffer, push.region, self.h2d_stream)
                     self.mark_transfer(push, push.dst, t)
                 continue
             if src_l and dst_l:
@@ -1244,10 +1250,23 @@ class Session:
     def results(self, gather: str = "root", out: Optional[dict] = None):
         """Final buffers: each final piece from its lowest-id holder
         (simulator.py:210-222).  Call after ``synchronize``."""
+        return self.finish_results(self.issue_results(gather, out, join=False))
+
+    def issue_results(self, gather: str = "root", out: Optional[dict] = None, join: bool = True):
+        """Post the read-back of the final buffers on the read-back stream
+        (asynchronous; ``join`` first orders it after all work issued so far
+        on every stream).  ``finish_results`` completes it."""
         self.gather = gather
         out_arrays = out or {}
         if gather == "none":
-            return {}
+            return None
+        if join:
+            for d in self.devices:
+                for st in N.ALL_STREAMS:
+                    if st != self.d2h_stream:
+                        ev = self.event(d)
+                        N.call("cq_event_record", ctypes.c_uint64(ev), d, st)
+                        N.call("cq_stream_wait_event", d, self.d2h_stream, ctypes.c_uint64(ev))
         out = {}
         root = self.pl.rank == 0
         pending = []
@@ -1298,6 +1317,7 @@ class Session:
             if span is not None:
                 temp_pins.append(span)
         bounced = []
+        st = self.d2h_stream
         for view, arr, region in direct:
             ha = N.box3((0,) * arr.ndim, arr.shape)
             for box in region.boxes:
@@ -1305,18 +1325,27 @@ class Session:
                 if _needs_bounce(arr, box):
                     tmp = np.empty(box.shape, dtype=arr.dtype)
                     bounced.append((arr, box, tmp))
-                    N.call("cq_copy_box_d2h", view.device, N.STREAM_COMM, view.itemsize,
+                    N.call("cq_copy_box_d2h", view.device, st, view.itemsize,
                            ctypes.c_void_p(tmp.ctypes.data), ctypes.byref(cb), ctypes.byref(view.c),
                            ctypes.byref(cb))
                     continue
-                N.call("cq_copy_box_d2h", view.device, N.STREAM_COMM, view.itemsize,
+                N.call("cq_copy_box_d2h", view.device, st, view.itemsize,
                        ctypes.c_void_p(arr.ctypes.data), ctypes.byref(ha), ctypes.byref(view.c),
                        ctypes.byref(cb))
         remote = [p for p in pending if p[0] == "nccl"]
         if remote:
+            if st != N.STREAM_COMM:
+                raise ValidationError("gather='root' across ranks reads back on the comm stream")
             self.gather_remote(remote, bounced)
+        return (out, bounced, temp_pins, root)
+
+    def finish_results(self, state):
+        """Wait for ``issue_results``' copies and return the buffers."""
+        if state is None:
+            return {}
+        out, bounced, temp_pins, root = state
         for d in self.devices:
-            N.call("cq_stream_synchronize", d, N.STREAM_COMM)
+            N.call("cq_stream_synchronize", d, self.d2h_stream)
         for arr, box, tmp in bounced:
             arr[tuple(slice(lo, hi) for lo, hi in zip(box.mins, box.maxs))] = tmp
         for span in temp_pins:
@@ -1324,6 +1353,26 @@ class Session:
         if self.gather == "root" and not root:
             return {}
         return out
+
+    def set_inputs(self, arrays: dict):
+        """Host contents of array-initialised buffers for the next
+        ``execute(upload=True)`` (same shape and element kind)."""
+        for name, arr in arrays.items():
+            b = self.buffers[name]
+            if b.init.kind != "array":
+                raise ValidationError(f"buffer '{name}' is not array-initialised")
+            a = np.ascontiguousarray(arr, dtype=b.dtype)
+            if a.shape != b.extent.shape:
+                raise ValidationError(f"buffer '{name}': input shape {a.shape} != {b.extent.shape}")
+            self.host_init[name] = a
+            self._overridden.add(name)
+        self.pin_inputs()
+
+    def reset_inputs(self):
+        """Back to the plan's own initial contents after ``set_inputs``."""
+        for name in self._overridden:
+            self.host_init.pop(name, None)
+        self._overridden = set()
 
     def gather_remote(self, items, bounced):
         """Ship final pieces held by other ranks to rank 0 over NCCL."""
@@ -1493,3 +1542,48 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
     finally:
         session.close()
     return RunResult(buffers=buffers, trace=events, makespan=makespan, plan=plan, measured=measured)
+
+
+def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Placement] = None):
+    """Run ``plan`` once per job with two executions in flight: while one
+    simulation computes and its results travel back (device->host), the next
+    one's inputs travel in (host->device) -- the copy engines of both PCIe
+    directions and the SMs work at once.  Each job is ``(inputs, out)``:
+    ``inputs`` {buffer: host array} (None: the plan's own initial arrays) and
+    ``out`` {buffer: destination array} (None: fresh arrays).  Returns the list
+    of per-job buffer dicts, as ``run(...).buffers``.  Results are identical to
+    calling ``run`` per job."""
+    if gather not in ("root", "local", "none"):
+        raise ValidationError(f"unknown gather mode '{gather}'")
+    sessions = [Session(plan, placement, trace=False,
+                        copy_streams=(N.STREAM_LANE0 + 2 * i, N.STREAM_LANE0 + 2 * i + 1)) for i in range(2)]
+    if sessions[0].pl.world > 1 and gather == "root":
+        for s in sessions:
+            s.close()
+        raise ValidationError("run_batch across ranks reads back locally: use gather='local' or 'none'")
+    results = [None] * len(jobs)
+    inflight = [None, None]
+    try:
+        for k, (inputs, out) in enumerate(jobs):
+            slot = k % 2
+            s = sessions[slot]
+            if inflight[slot] is not None:
+                idx, state = inflight[slot]
+                results[idx] = s.finish_results(state)
+                s.check_errors()
+                s.recycle()
+            if inputs:
+                s.set_inputs(inputs)
+            elif s._overridden:
+                s.reset_inputs()
+            s.execute(upload=True)
+            inflight[slot] = (k, s.issue_results(gather, out))
+        for slot in sorted(range(2), key=lambda t: inflight[t][0] if inflight[t] else -1):
+            if inflight[slot] is not None:
+                idx, state = inflight[slot]
+                results[idx] = sessions[slot].finish_results(state)
+                sessions[slot].synchronize()
+    finally:
+        for s in sessions:
+            s.close()
+    return results

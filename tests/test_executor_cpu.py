@@ -345,3 +345,22 @@ def test_fused_wave_chain_float64(fake):
     s.close()
     u, up = onat.wave_run(u0, u0, steps, 0.3)
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
+def test_run_batch_matches_run(fake):
+    """run_batch (two sessions in flight, their own upload / read-back
+    streams) returns, per job, exactly what run() returns -- including jobs
+    with their own input arrays."""
+    from oracle import native as onat
+    fake(1)
+    h, w, steps = 96, 32, 10
+    u0 = np.random.default_rng(51).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=steps, kind="float32", u0=u0, up0=u0)
+    plan = cq.generate_commands(prog.graph(), 2)
+    other = np.random.default_rng(52).uniform(0, 1, (h, w)).astype(np.float32)
+    jobs = [(None, None), ({"u": other, "up": other}, None), (None, None), (None, None)]
+    res = E.run_batch(plan, jobs, placement=E.Placement(1, 0, (0,)))
+    for (inp, _o), r in zip(jobs, res):
+        src = u0 if inp is None else other
+        u, up = onat.wave_run(src, src, steps, 0.25)
+        assert dsl.same_bits(r["u"], u) and dsl.same_bits(r["up"], up)
