@@ -343,3 +343,19 @@ def test_graph_replay_equals_plain_replay(nodes):
         s.close()
     for o in out[1:]:
         assert dsl.same_bits(out[0]["u"], o["u"]) and dsl.same_bits(out[0]["up"], o["up"])
+
+
+def test_run_batch_two_in_flight_matches_oracle():
+    """run_batch (upload of job k+1 overlapping kernels and read-back of job
+    k, separate copy streams per session) == the oracle per job."""
+    from paper_2505_06022_b200.executor import run_batch
+    h, w, steps = 515, 640, 22
+    a = np.random.default_rng(61).uniform(0, 1, (h, w)).astype(np.float32)
+    b = np.random.default_rng(62).uniform(0, 1, (h, w)).astype(np.float32)
+    plan = cq.generate_commands(W.wave_program(h, w, steps=steps, kind="float32", u0=a, up0=a).graph(), 2)
+    jobs = [(None, None), ({"u": b, "up": b}, None), (None, None), ({"u": b, "up": a}, None), (None, None)]
+    res = run_batch(plan, jobs)
+    for (inp, _o), r in zip(jobs, res):
+        u0, up0 = (a, a) if inp is None else (inp["u"], inp["up"])
+        u, up = onat.wave_run(u0, up0, steps, 0.25)
+        assert dsl.same_bits(r["u"], u) and dsl.same_bits(r["up"], up)
