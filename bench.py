@@ -518,6 +518,11 @@ def bench_kernels(args, dist, placement, peaks):
                       "chunks": nodes, "launches_per_pass": k[2] // 20,
                       "note": ("BASELINE config 0: 2^24 x fp32, 192 MiB per pass (> 126 MB L2; "
                                "back-to-back passes partly hit L2)") if n == 1 << 24 else "inputs > L2"}
+        if args.energy and n == 1 << 28:
+            e = energy_loop(sess, dist, ms / 20, 1.0)
+            if e and "j_per_iter" in e:
+                e["gb_per_joule"] = 12 * n / 1e9 / e["j_per_iter"]
+            out[label]["energy"] = e
         sess.close()
 
     # wave variants: float64 (the reference's own element kind, 24 B/cell/step,
@@ -604,6 +609,11 @@ def bench_kernels(args, dist, placement, peaks):
                                  "peak_sustained": sustained, "frac_sustained": kern_tflops / sustained,
                                  "peak_definition": "measured bf16 dense (burst | sustained) / 2 (TF32) "
                                                     "/ 3 (products)"}
+        if args.energy and variant == "3xtf32":
+            e = energy_loop(sess, dist, ms / 3, 1.0)
+            if e and "j_per_iter" in e:
+                e["tflop_per_joule"] = 2 * m ** 3 / 1e12 / e["j_per_iter"]
+            entry["energy"] = e
         out[f"sgemm_{variant}_{m}"] = entry
         sess.close()
     return out
