@@ -590,14 +590,34 @@ __device__ __forceinline__ double2 wave_vec(double2 m, double2 n, double2 s, dou
 }
 
 __device__ __forceinline__ float4 wave_vec(float4 m, float4 n, float4 s, float4 p, float wv, float ev, float c) {
-  const f32x2 mid = pack2(m.y, m.z);  // east of A == west of B
-  const f32x2 oA = wave_pair(pack2(m.x, m.y), pack2(n.x, n.y), pack2(s.x, s.y), pack2(wv, m.x), mid,
-                             pack2(p.x, p.y), c);
-  const f32x2 oB = wave_pair(pack2(m.z, m.w), pack2(n.z, n.w), pack2(s.z, s.w), mid, pack2(m.w, ev),
-                             pack2(p.z, p.w), c);
+  // n + s on the aligned halves of the float4s (packed, no register moves);
+  // + w and + e as scalar adds on the lanes' own registers (the neighbour
+  // pairs (w, x), (y, z), (w, e) straddle the register pairs); the rest packed
+  const f32x2 nsA = add2(pack2(n.x, n.y), pack2(s.x, s.y));
+  const f32x2 nsB = add2(pack2(n.z, n.w), pack2(s.z, s.w));
+  float a0, a1, b0, b1;
+  unpack2(nsA, a0, a1);
+  unpack2(nsB, b0, b1);
+  a0 = __fadd_rn(__fadd_rn(a0, wv), m.y);
+  a1 = __fadd_rn(__fadd_rn(a1, m.x), m.z);
+  b0 = __fadd_rn(__fadd_rn(b0, m.y), m.w);
+  b1 = __fadd_rn(__fadd_rn(b1, m.z), ev);
+  const f32x2 uA = pack2(m.x, m.y), uB = pack2(m.z, m.w);
+  const f32x2 u2A = add2(uA, uA), u2B = add2(uB, uB);
+  const f32x2 lapA = sub2(pack2(a0, a1), add2(u2A, u2A));
+  const f32x2 lapB = sub2(pack2(b0, b1), add2(u2B, u2B));
+  float l0, l1, l2, l3;
+  unpack2(lapA, l0, l1);
+  unpack2(lapB, l2, l3);
+  const f32x2 tA = sub2(u2A, pack2(p.x, p.y)), tB = sub2(u2B, pack2(p.z, p.w));
+  float t0, t1, t2, t3;
+  unpack2(tA, t0, t1);
+  unpack2(tB, t2, t3);
   float4 o;
-  unpack2(oA, o.x, o.y);
-  unpack2(oB, o.z, o.w);
+  o.x = __fadd_rn(t0, __fmul_rn(c, l0));
+  o.y = __fadd_rn(t1, __fmul_rn(c, l1));
+  o.z = __fadd_rn(t2, __fmul_rn(c, l2));
+  o.w = __fadd_rn(t3, __fmul_rn(c, l3));
   return o;
 }
 
@@ -967,8 +987,6 @@ int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const flo
     NB_LAUNCH(1)
     NB_LAUNCH(2)
     NB_LAUNCH(3)
-    NB_LAUNCH(6)
-    NB_LAUNCH(8)
     default:
     NB_LAUNCH(4)
 #undef NB_LAUNCH
