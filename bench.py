@@ -293,8 +293,14 @@ def bench_wave(args, dist, placement, peaks):
     dev_ms = dist.max(dev_ms)
     cells = H * Wd * steps * args.steps
     value = 12 * cells / (dev_ms / 1e3) / 1e9
-    achieved = kern_bytes / (kern_ms / 1e3) / 1e9
-    achieved = dist.min(achieved)
+    # roofline numerator per the contract: SURVEY §8d's algorithmic figure
+    # (12 B per cell per time step) x the units one launch processes (its
+    # cells x the time steps it advances); the kernel's own minimum traffic
+    # (16 B/cell per fused pass) is reported beside it
+    steps_per_launch = {"wave5_fused8": 8, "wave5_fused4": 4}.get(dom_kind, 1)
+    kern_s = kern_ms / 1e3
+    achieved = dist.min(12 * steps_per_launch * (kern_bytes / bpc) / kern_s / 1e9)
+    achieved_own = dist.min(kern_bytes / kern_s / 1e9)
     clk = clocks.summary()
 
     # ---- end to end through the public API, host buffers ------------------
@@ -346,14 +352,17 @@ def bench_wave(args, dist, placement, peaks):
                      "kernel": {"wave5_fused8": "wave5_fused_kernel<float,8,4,6,256> (8 time steps per pass)",
                                 "wave5_fused4": "wave5_fused_kernel<float,4,4,6,128> (4 time steps per pass)"}.get(
                                     dom_kind, "wave5_rows_kernel<float,32>"),
-                     "bytes_per_cell": bpc,
+                     "algorithmic_bytes_per_cell_step": 12, "time_steps_per_launch": steps_per_launch,
                      "cells_per_launch": dom_launch[1], "launches": len(dominant),
-                     "bytes_per_launch": bpc * dom_launch[1],
+                     "bytes_per_launch": 12 * steps_per_launch * dom_launch[1],
+                     "kernel_bytes_per_cell": bpc, "achieved_kernel_traffic": achieved_own,
+                     "frac_kernel_traffic": achieved_own / peaks[0]["hbm_gbs"],
                      "peak_source": peaks[1] + " hbm_gbs (torch copy)",
-                     "note": ("8 time steps per HBM pass: twice the arithmetic per byte of the 4-step pass; "
-                              "the kernel is FP32-pipe / issue limited (ncu: FMA pipe 63% active, issue slots "
-                              "64% busy; profiles/r01/wave5_fused8_ncu_full_summary.txt), so its HBM fraction is "
-                              "below 1 while the step is 1.3x faster than 4-step passes at 0.85 of HBM")
+                     "note": ("temporal blocking: one launch advances 8 time steps while reading X(t), X(t-1) "
+                              "and writing two levels (16 B/cell, ncu traffic above), so the algorithmic "
+                              "12 B/cell/step rate exceeds the HBM peak; the pass itself is FP32-pipe / issue "
+                              "limited (ncu: FMA pipe 63% active, issue 64% busy, "
+                              "profiles/r01/wave5_fused8_ncu_full_summary.txt)")
                              if dom_kind == "wave5_fused8" else None,
                      "launch_timing": timing_source},
         "clocks": clk,
