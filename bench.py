@@ -44,6 +44,7 @@ sys.path.insert(0, ROOT)
 
 SIZE = 16384
 WAVE_STEPS = 100
+SWEEP_SECONDS = 1.0   # NVML energy window per clock point
 C = 0.25
 
 
@@ -694,6 +695,43 @@ def reference_arm(args, dist):
     }
 
 
+def clock_sweep(args, dist, placement):
+    """SYnergy sweep (BASELINE config 4): J and seconds per iteration of the
+    100-step wave simulation and of 3 N-body steps at three SM clocks (max,
+    ~75%, ~50% of the supported list), the reference time model's beta fitted
+    per kernel, and the reference selection rule per target over the measured
+    points.  Locking clocks changes shared hardware state, so it runs only
+    with CQ_ALLOW_CLOCK_LOCK=1 (libcq refuses otherwise) and at N = 1."""
+    if os.environ.get("CQ_ALLOW_CLOCK_LOCK") != "1":
+        return ("not run: SM clock locking is disabled on this shared pool (cq_nvml_lock_sm_clock "
+                "requires CQ_ALLOW_CLOCK_LOCK=1); J/iteration reported at the running clock")
+    if dist.world != 1:
+        return "not run: the sweep is a 1-GPU measurement"
+    import paper_2505_06022_b200 as cq
+    from paper_2505_06022_b200 import executor as E, synergy as S, workloads as W
+    from paper_2505_06022_b200.energy import EnergyTarget
+    dev = placement.devices[0]
+    clocks = S.sweep_clocks(S.supported_sm_clocks(dev))
+    out = {"clocks_mhz": clocks}
+    u0, up0 = wave_inputs(args.size, args.size, (0, args.size))
+    programs = {"wave5_100_steps": W.wave_program(args.size, args.size, steps=args.wave_steps, c=C, u0=u0, up0=up0),
+                "nbody_3_steps": W.nbody_program(args.nbody, steps=3)}
+    for name, prog in programs.items():
+        sess = E.Session(cq.generate_commands(prog.graph(), 1), placement, trace=False)
+        sess.execute(upload=True)
+        sess.synchronize()
+        sess.recycle()
+        sess.capture()
+        mk = S.sweep(name, lambda: sess.replay(1), dev, clocks, seconds=SWEEP_SECONDS, sync=sess.synchronize)
+        entry = {"points": {str(m): {"s_per_iter": t, "j_per_iter": j} for m, (t, j) in sorted(mk.points.items())}}
+        if len(mk.points) > 1:
+            entry["beta"] = float(S.fit_beta(mk))
+            entry["selected_mhz"] = {t.value: S.select_measured(mk, t) for t in EnergyTarget}
+        out[name] = entry
+        sess.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -753,9 +791,7 @@ def main():
             "e2e": wave["e2e"], "roofline": wave["roofline"], "cpu_baseline": cpu,
             "clocks": wave["clocks"], "gpu_launches": wave["gpu_launches"],
             "energy": {"wave5": wave["energy"],
-                       "clock_sweep": "not run: SM clock locking is disabled on this shared pool "
-                                      "(cq_nvml_lock_sm_clock requires CQ_ALLOW_CLOCK_LOCK=1); "
-                                      "J/iteration reported at the running clock"},
+                       "clock_sweep": clock_sweep(args, dist, placement) if args.energy else None},
             "kernels": kernels,
         }
         print(json.dumps(line))

@@ -122,3 +122,37 @@ def sweep(name, fn, device=0, clocks=None, seconds=1.0, sync=None) -> MeasuredKe
         r = kernel_energy(fn, device, seconds, sync)
         mk.points[r["sm_mhz"]] = (r["s_per_call"], r["j_per_call"])
     return mk
+
+
+def sweep_clocks(supported, fractions=(1.0, 0.75, 0.5)) -> list:
+    """The supported SM clocks nearest to the given fractions of the highest
+    one (BASELINE: "e.g. max, ~75%, ~50%"), highest first, distinct."""
+    if not supported:
+        return []
+    top = max(supported)
+    out = []
+    for f in fractions:
+        c = min(supported, key=lambda m: (abs(m - f * top), -m))
+        if c not in out:
+            out.append(c)
+    return out
+
+
+def fit_beta(kernel: MeasuredKernel) -> Fraction:
+    """Least-squares beta of the reference time model (energy.py:74-78)
+    t(f) = t_ref * (beta + (1 - beta) * f_ref / f) with f_ref the highest
+    measured clock and t_ref its time: beta ~ 1 for a memory-bound kernel
+    (time independent of the SM clock), ~ 0 for a compute-bound one."""
+    levels = kernel.levels()
+    if len(levels) < 2:
+        raise ValidationError(f"kernel '{kernel.name}': beta needs >= 2 measured clocks")
+    f_ref = Fraction(levels[-1])
+    t_ref = Fraction(kernel.points[levels[-1]][0])
+    # t/t_ref - f_ref/f = beta * (1 - f_ref/f)  ->  one-parameter least squares
+    num = den = Fraction(0)
+    for mhz in levels[:-1]:
+        x = 1 - f_ref / Fraction(mhz)
+        y = Fraction(kernel.points[mhz][0]) / t_ref - f_ref / Fraction(mhz)
+        num += x * y
+        den += x * x
+    return num / den

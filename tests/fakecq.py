@@ -418,6 +418,71 @@ class FakeLib:
     cq_nvml_lock_sm_clock = cq_nvml_reset_sm_clock = _nvml_absent
 
 
+class FakeNvmlLib(FakeLib):
+    """FakeLib plus a simulated NVML device: a lockable SM clock and an
+    energy counter integrating P(f) = static + dynamic * (f / f_max)^3 over
+    wall time (for the SYnergy sweep logic on CPU)."""
+
+    CLOCKS = (1965, 1800, 1500, 1200, 990, 600)
+
+    def __init__(self, *a, allow_lock=True, **kw):
+        super().__init__(*a, **kw)
+        import time as _t
+        self._t = _t
+        self.mhz = max(self.CLOCKS)
+        self.allow_lock = allow_lock
+        self._mj = 0.0
+        self._last = _t.perf_counter()
+
+    def _power_w(self):
+        return 200.0 + 800.0 * (self.mhz / max(self.CLOCKS)) ** 3
+
+    def _advance(self):
+        now = self._t.perf_counter()
+        self._mj += self._power_w() * (now - self._last) * 1000.0
+        self._last = now
+
+    def cq_nvml_init(self):
+        return 0
+
+    def cq_nvml_energy_mj(self, d, p):
+        self._advance()
+        _obj(p).value = int(self._mj)
+        return 0
+
+    def cq_nvml_power_mw(self, d, p):
+        _obj(p).value = int(self._power_w() * 1000)
+        return 0
+
+    def cq_nvml_sm_clock_mhz(self, d, cur, mx):
+        _obj(cur).value, _obj(mx).value = self.mhz, max(self.CLOCKS)
+        return 0
+
+    def cq_nvml_throttle_reasons(self, d, p):
+        _obj(p).value = 0
+        return 0
+
+    def cq_nvml_supported_sm_clocks(self, d, buf, n):
+        arr = _obj(buf)
+        for i, c in enumerate(self.CLOCKS):
+            arr[i] = c
+        _obj(n).value = len(self.CLOCKS)
+        return 0
+
+    def cq_nvml_lock_sm_clock(self, d, mhz):
+        if not self.allow_lock:
+            self.err = b"clock locking disabled (CQ_ALLOW_CLOCK_LOCK)"
+            return N.CQ_ERR_PERMISSION
+        self._advance()
+        self.mhz = int(_val(mhz))
+        return 0
+
+    def cq_nvml_reset_sm_clock(self, d):
+        self._advance()
+        self.mhz = max(self.CLOCKS)
+        return 0
+
+
 class LocalTransport:
     """Single process: NCCL ops must never be issued."""
 

@@ -55,3 +55,57 @@ def test_select_measured_matches_model_selection_on_model_points():
             for target in cq.EnergyTarget:
                 want = cq.select_frequency(dev, target, t_ref, beta)
                 assert select_measured(k, target) == int(want * 1000)
+
+
+def test_sweep_fit_and_select_on_a_simulated_nvml_device(monkeypatch):
+    """SYnergy sweep logic on CPU: three clocks (max, ~75 %, ~50 %) of the
+    supported list, a compute-bound and a memory-bound 'kernel' (time ~ 1/f
+    vs constant), the reference time model's beta fitted from the measured
+    points, and the reference selection rule over them."""
+    import time as _t
+    from fakecq import FakeNvmlLib
+    from paper_2505_06022_b200 import _native as N
+    from paper_2505_06022_b200 import synergy as S
+    from paper_2505_06022_b200.energy import EnergyTarget
+    lib = FakeNvmlLib(1)
+    monkeypatch.setattr(N, "_lib", lib)
+    clocks = S.sweep_clocks(S.supported_sm_clocks(0))
+    assert clocks == [1965, 1500, 990]
+    compute = S.sweep("compute", lambda: _t.sleep(0.008 * 1965 / lib.mhz), 0, clocks, seconds=0.25)
+    memory = S.sweep("memory", lambda: _t.sleep(0.008), 0, clocks, seconds=0.25)
+    assert compute.levels() == memory.levels() == [990, 1500, 1965]
+    assert lib.mhz == 1965  # clocks reset after the sweep
+    assert abs(float(S.fit_beta(compute))) < 0.3 and abs(float(S.fit_beta(memory)) - 1) < 0.3
+    # a memory-bound kernel saves energy at a low clock at no time cost
+    assert S.select_measured(memory, EnergyTarget.MIN_ENERGY) == 990
+    assert S.select_measured(memory, EnergyTarget.MAX_PERF) == 1965
+    # without permission only the running clock is measured
+    lib.allow_lock = False
+    only = S.sweep("memory", lambda: _t.sleep(0.002), 0, clocks, seconds=0.05)
+    assert only.levels() == [1965]
+
+
+def test_bench_clock_sweep_leg_on_the_simulated_device(monkeypatch):
+    """bench.py's SYnergy leg end to end on the CPU double: three clocks per
+    kernel, beta and per-target selections reported; without
+    CQ_ALLOW_CLOCK_LOCK it reports why it did not run."""
+    import types
+    import bench
+    from fakecq import FakeNvmlLib
+    from paper_2505_06022_b200 import _native as N
+    from paper_2505_06022_b200 import executor as E
+    lib = FakeNvmlLib(1)
+    monkeypatch.setattr(N, "_lib", lib)
+    args = types.SimpleNamespace(size=64, wave_steps=8, nbody=256)
+    dist = types.SimpleNamespace(world=1, rank=0)
+    pl = E.Placement(1, 0, (0,))
+    monkeypatch.delenv("CQ_ALLOW_CLOCK_LOCK", raising=False)
+    assert bench.clock_sweep(args, dist, pl).startswith("not run")
+    monkeypatch.setenv("CQ_ALLOW_CLOCK_LOCK", "1")
+    monkeypatch.setattr(bench, "SWEEP_SECONDS", 0.05)
+    out = bench.clock_sweep(args, dist, pl)
+    assert out["clocks_mhz"] == [1965, 1500, 990]
+    for name in ("wave5_100_steps", "nbody_3_steps"):
+        assert len(out[name]["points"]) == 3
+        assert set(out[name]["selected_mhz"]) == {"MAX_PERF", "MIN_ENERGY", "MIN_EDP", "MIN_ED2P"}
+        assert out[name]["selected_mhz"]["MAX_PERF"] == 1965
