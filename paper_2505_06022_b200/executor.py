@@ -419,10 +419,15 @@ class Session:
         self.host_init = {}
         self._overridden = set()
         self._sched = None
+        self._raw = None        # the plan's schedule before fusion (schedule())
+        self._lanes = None      # node -> compute stream (lane())
+        self._exec_of = None    # (task id, node) -> ExecuteCommand (exec_fused)
+        self._halo_marks = []   # trace marks of a fused block's halo transfers
         self.t0 = None
         self._t0 = {}
         self.uploading = True
         self.bounce = []        # temporaries of bounced host copies (kept until sync)
+        kahn_order(plan)  # validates acyclicity before touching devices
         for d in self.devices:
             N.call("cq_init_device", d)
         # several GPUs in one process: box copies between them go peer to
@@ -432,7 +437,6 @@ class Session:
                 if d != e:
                     ok = ctypes.c_int32()
                     N.call("cq_enable_peer", d, e, ctypes.byref(ok))
-        kahn_order(plan)  # validates acyclicity before touching devices
         self.alt = {}
         self.chains = fusion.find_chains(plan, self._raw_schedule())
         self.allocate()
@@ -720,7 +724,7 @@ class Session:
         """Compute stream of a node: with several local nodes on one device
         (independent allocations) each gets its own lane, so their executes
         run concurrently; otherwise the compute stream."""
-        lanes = getattr(self, "_lanes", None)
+        lanes = self._lanes
         if lanes is None:
             lanes = self._lanes = {}
             by_dev = {}
@@ -806,7 +810,7 @@ class Session:
                         break
         ext = _cbox(b.extent)
         W = ch.W
-        if not hasattr(self, "_exec_of"):
+        if self._exec_of is None:
             self._exec_of = {(c.task_id, c.node): c for c in self.plan.commands if isinstance(c, ExecuteCommand)}
         for node in sorted(ch.rows):
             if not self.local(node):
@@ -1039,7 +1043,7 @@ class Session:
         return self._sched
 
     def _raw_schedule(self):
-        if getattr(self, "_raw", None) is not None:
+        if self._raw is not None:
             return self._raw
         # Task-major order: every push of a task depends only on commands of
         # earlier tasks (producers are read from the table state before the
