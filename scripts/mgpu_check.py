@@ -54,6 +54,30 @@ def main():
                       dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up))
     os.environ.pop("CQ_WAVE_FUSE")
 
+    # float64 (the reference's kind) chain, temporally blocked across ranks
+    d0 = np.random.default_rng(4).uniform(0, 1, (h, w))
+    prog = W.wave_program(h, w, steps=18, kind="float64", c=0.3, u0=d0, up0=d0)
+    res = E.run(cq.generate_commands(prog.graph(), world), placement=pl)
+    if rank == 0:
+        u, up = onat.wave_run(d0, d0, 18, 0.3)
+        check(f"wave float64 {h}x{w}x18 nodes={world}",
+              dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up))
+
+    # run_batch across ranks: two simulations in flight, each rank reads back its rows
+    prog = W.wave_program(h, w, steps=12, kind="float32", u0=u0, up0=up0)
+    plan = cq.generate_commands(prog.graph(), world)
+    batch = E.run_batch(plan, [(None, None), ({"u": up0, "up": u0}, None), (None, None)], gather="local")
+    mine = next(c for c in plan.commands if type(c).__name__ == "ExecuteCommand" and c.node == rank)
+    lo, hi = mine.chunk.box.mins[0], mine.chunk.box.maxs[0]
+    ok = True
+    for (inp, _o), r in zip([(None, None), ({"u": up0, "up": u0}, None), (None, None)], batch):
+        a, b = (u0, up0) if inp is None else (up0, u0)
+        u, up = onat.wave_run(a, b, 12, 0.25)
+        ok = ok and dsl.same_bits(r["u"][lo:hi], u[lo:hi]) and dsl.same_bits(r["up"][lo:hi], up[lo:hi])
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    check(f"run_batch 3 jobs nodes={world} (every rank's own rows)", bool(flag.item()))
+
     # SAXPY, BASELINE config 1 shape scaled
     n = (1 << 22) + 5
     x, y = W.saxpy_inputs(n, "float32", seed=0)
