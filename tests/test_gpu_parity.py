@@ -359,3 +359,23 @@ def test_run_batch_two_in_flight_matches_oracle():
         u0, up0 = (a, a) if inp is None else (inp["u"], inp["up"])
         u, up = onat.wave_run(u0, up0, steps, 0.25)
         assert dsl.same_bits(r["u"], u) and dsl.same_bits(r["up"], up)
+
+
+def test_wave_baseline_size_bit_exact():
+    """BASELINE config 1 at full size: 16384 x 16384 fp32, 100 steps,
+    temporally blocked (11 eight-step + 3 four-step passes) on one GPU and
+    on 4 nodes sharing it (KL-row halo exchanges between the slabs), against
+    the OpenMP oracle of the per-step tree -- bit for bit."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    n, steps = 16384, 100
+    u0 = W.wave_pulse(n, n, "float32")
+    u, up = onat.wave_run(u0, u0, steps, 0.25)
+    for nodes in (1, 4):
+        prog = W.wave_program(n, n, steps=steps, kind="float32", c=0.25, u0=u0, up0=u0)
+        s = Session(cq.generate_commands(prog.graph(), nodes), Placement(1, 0, (0,)), trace=False)
+        assert [b.kl for b in s.chains[0].blocks] == [8] * 11 + [4] * 3
+        s.execute(upload=True)
+        s.synchronize()
+        res = s.results()
+        s.close()
+        assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up), nodes
