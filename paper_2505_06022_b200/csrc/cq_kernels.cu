@@ -645,6 +645,14 @@ __device__ __forceinline__ void cp_async_wait() {
 // slower (profiles/r01/fused_cfg_sweep.log).
 template <int KL, int V>
 struct FusedShape {
+  // kOldInSmem keeps the rows two iterations old of every level in shared
+  // memory (each is read once more, as the north neighbour one level up and
+  // as u_prev two levels up), freeing ~32 registers: for KL = 8, V = 4 that
+  // fits two 6-warp blocks per SM without spills, but measured slower
+  // (16.7 vs 20.8 TB/s: the extra LDS/STS per level cost more than the 12
+  // warps gain), so the register-only variant runs one 8-warp block per SM
+  // (~200 registers).
+  static constexpr bool kOldInSmem = false;
   static constexpr int kWarps = 8;
   static constexpr int kMinBlocks = (KL == 8 && V == 4) ? 1 : 2;
 };
@@ -659,7 +667,11 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   constexpr int SW = 32 * V - 2 * KL;
   extern __shared__ __align__(16) uint8_t fused_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr bool OLD_SM = FusedShape<KL, V>::kOldInSmem;
+  constexpr int WPB_ = FusedShape<KL, V>::kWarps;
   Vec* ring = reinterpret_cast<Vec*>(fused_smem) + (size_t)warp * D * 2 * 32;  // [D][2][32]
+  // [KL][3][32] per warp after all rings: level j's rows by slot (OLD_SM only)
+  Vec* olds = reinterpret_cast<Vec*>(fused_smem) + (size_t)WPB_ * D * 2 * 32 + (size_t)warp * KL * 3 * 32;
   const int64_t strip = (int64_t)blockIdx.x * FusedShape<KL, V>::kWarps + warp;
   const int64_t r0 = out_lo + (int64_t)blockIdx.y * RB;
   if (strip * SW >= W || r0 >= out_hi) return;  // warp-uniform
@@ -712,13 +724,16 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
       cp_async_wait<D - 1>();  // row ri (the oldest group) has landed
       L[0][s] = ring[(sd * 2 + 0) * 32 + lane];
       P[s] = ring[(sd * 2 + 1) * 32 + lane];
+      if (OLD_SM) olds[(0 * 3 + s) * 32 + lane] = L[0][s];
       if (ri + D < re) fetch(sd, ri + D, ri + D - rb);
       cp_async_commit();
+      // the row two iterations old of level k (north of level k+1, u_prev of k+2)
+      auto old_of = [&](int k) -> Vec { return OLD_SM ? olds[(k * 3 + so) * 32 + lane] : L[k][so]; };
 #pragma unroll
       for (int j = 1; j <= KL; ++j) {
         const int64_t rho = ri - j;
         const Vec mid = L[j - 1][sm];
-        Vec nn = L[j - 1][so], ss = L[j - 1][s];
+        Vec nn = old_of(j - 1), ss = L[j - 1][s];
         T wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
         T ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
         if (EDGE) {
@@ -727,9 +742,12 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
           if (col == 0) wv = first_of(mid);
           if (col + V == W) ev = last_of(mid);
         }
-        const Vec pp = (j == 1) ? P[sm] : L[j >= 2 ? j - 2 : 0][so];
+        const Vec pp = (j == 1) ? P[sm] : old_of(j >= 2 ? j - 2 : 0);
         const Vec o = wave_vec(mid, nn, ss, pp, wv, ev, c);
-        if (j < KL) L[j][s] = o;
+        if (j < KL) {
+          L[j][s] = o;
+          if (OLD_SM) olds[(j * 3 + s) * 32 + lane] = o;
+        }
         if (j == KL - 1 && rho >= r0 && rho < r1) {
           if (keep) __stcs(reinterpret_cast<Vec*>(sp), o);
           sp += pstr;
@@ -766,7 +784,7 @@ static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& up
   constexpr int WPB = FusedShape<KL, V>::kWarps;
   dim3 grid((unsigned)((strips + WPB - 1) / WPB), (unsigned)((out_hi - out_lo + RB - 1) / RB));
   auto kern = wave5_fused_kernel<T, KL, V, D, RB>;
-  const int smem = WPB * D * 2 * 32 * V * (int)sizeof(T);
+  const int smem = WPB * (D * 2 + (FusedShape<KL, V>::kOldInSmem ? KL * 3 : 0)) * 32 * V * (int)sizeof(T);
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4);
   return CQ_OK;
