@@ -161,7 +161,7 @@ int cq_saxpy(int device, int stream, int kind, double alpha, int64_t ialpha, con
 int cq_wave5(int device, int stream, int kind, const cq_view_t* u, const cq_view_t* upr,
              const cq_view_t* out, const cq_box_t* box, const cq_box_t* extent, double c,
              double k2, double k4);
-/* KL (4 or 8; float64: 4) wave steps in one HBM pass (temporal blocking): from u = X(t)
+/* KL (4 or 8) wave steps in one HBM pass (temporal blocking): from u = X(t)
  * and upr = X(t-1), readable on rows [in_lo, in_hi), write X(t+KL) to
  * out_last and X(t+KL-1) to out_prev on rows [out_lo, out_hi) x all columns.
  * Bit-identical to KL cq_wave5 launches (same per-cell tree and rounding).

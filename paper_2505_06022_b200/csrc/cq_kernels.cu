@@ -654,7 +654,7 @@ struct FusedShape {
   // (~200 registers).
   static constexpr bool kOldInSmem = false;
   static constexpr int kWarps = 8;
-  static constexpr int kMinBlocks = (KL == 8 && V == 4) ? 1 : 2;
+  static constexpr int kMinBlocks = KL == 8 ? 1 : 2;
 };
 
 template <typename T, int KL, int V, int D, int RB>
@@ -917,10 +917,14 @@ int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t
   const int cfg = cfg_env ? cfg_env : (levels == 8 ? 4 * 10000 + 6 * 1000 + 256 : 4 * 10000 + 6 * 1000 + 128);
   int status;
   if (kind == CQ_F64) {
-    // two doubles per lane (16-byte rows), 56 valid columns per warp strip
-    CQ_REQUIRE(levels == 4, "cq_wave5_fused: float64 runs 4 steps per pass");
-    status = launch_fused<double, 4, 2, 6, 128>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, H,
-                                                W, c, k2, k4);
+    // two doubles per lane (16-byte rows): 56 (KL = 4) or 48 (KL = 8) valid
+    // columns per warp strip
+    if (levels == 4)
+      status = launch_fused<double, 4, 2, 6, 128>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi,
+                                                  H, W, c, k2, k4);
+    else
+      status = launch_fused<double, 8, 2, 6, 256>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi,
+                                                  H, W, c, k2, k4);
     if (status != CQ_OK) return status;
     CQ_CHECK_LAUNCH();
     return CQ_OK;

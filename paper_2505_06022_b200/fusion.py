@@ -20,8 +20,8 @@ What changes against executing the plan command by command: the plan's
 one-row halo pushes of the fused tasks are replaced by one KL-row exchange
 per block; the last task's pushes are still posted after the chain, so every
 halo row the plan's ``final_locations`` lists holds its final version.
-float32 chains run KL = 8 blocks (half the bytes per step of KL = 4) with
-KL = 4 blocks where the parity needs them: an even number of out-of-place
+Chains run KL = 8 blocks (half the bytes per step of KL = 4) with KL = 4
+blocks where the parity needs them: an even number of out-of-place
 blocks keeps the current allocations where a CUDA-graph capture found them;
 leftover steps (< 4) run one step at a time.
 
@@ -173,23 +173,17 @@ def _halo_pushes_ok(pushes, ubuf, rows, W):
 
 def _blocks(tids, kind="float32"):
     """Split a chain into out-of-place blocks with an even count (so the
-    current allocations return to where they started): float32 uses as many
-    KL=8 blocks as the parity allows plus KL=4 blocks (KL=8 moves half the
-    bytes per step); float64 uses KL=4 only, four plain steps fixing an odd
-    count.  Tasks left over (< 4) run plain."""
+    current allocations return to where they started): as many KL=8 blocks
+    as the parity allows (KL=8 moves half the bytes per step of KL=4) plus
+    KL=4 blocks.  Tasks left over (< 4) run plain."""
     q, _r = divmod(len(tids), KL_BASE)   # quarter blocks
-    if kind == "float32":
-        b = q % 2                          # KL=4 blocks (same parity as q)
-        a = (q - b) // 2                   # KL=8 blocks
-        if (a + b) % 2:
-            a, b = a - 1, b + 2
-        if a < 0:
-            return [], tuple(tids)
-        sizes = [KL_PARITY] * a + [KL_BASE] * b
-    else:
-        if q % 2 == 1:
-            q -= 1
-        sizes = [KL_BASE] * q
+    b = q % 2                          # KL=4 blocks (same parity as q)
+    a = (q - b) // 2                   # KL=8 blocks
+    if (a + b) % 2:
+        a, b = a - 1, b + 2
+    if a < 0:
+        return [], tuple(tids)
+    sizes = [KL_PARITY] * a + [KL_BASE] * b
     if not sizes:
         return [], tuple(tids)
     blocks, i = [], 0

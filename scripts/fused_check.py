@@ -133,5 +133,49 @@ for kl in (4, 8):
         ms = ev[0].elapsed_time(ev[1])
         print(f"fused KL={kl} {steps} steps: {ms:.2f} ms = {12 * h * w * steps / ms / 1e6:.0f} GB/s effective "
               f"({16 * h * w * (steps // kl) / ms / 1e6:.0f} GB/s of 16 B/cell/pass)", flush=True)
+# FLOAT64: the fused double kernel (two doubles per lane) against one-step launches
+def view64(t, h, w):
+    return view(t, h, w)
+
+
+for (h, w) in [(517, 384), (300, 1024)]:
+    a = torch.rand((h, w), device="cuda", generator=g, dtype=torch.float64)
+    b = torch.rand((h, w), device="cuda", generator=g, dtype=torch.float64)
+    for kl in (4, 8):
+        x, y = a.clone(), b.clone()
+        ext = N.box3((0, 0), (h, w))
+        box = N.box3((0, 0), (h, w))
+        for _ in range(kl):
+            N.call("cq_wave5", 0, 0, N.CQ_F64, ctypes.byref(view(x, h, w)), ctypes.byref(view(y, h, w)),
+                   ctypes.byref(view(y, h, w)), ctypes.byref(box), ctypes.byref(ext), 0.3, K2, K4)
+            x, y = y, x
+        ol, op = torch.full_like(a, float("nan")), torch.full_like(a, float("nan"))
+        N.call("cq_wave5_fused", 0, 0, N.CQ_F64, kl, ctypes.byref(view(a, h, w)), ctypes.byref(view(b, h, w)),
+               ctypes.byref(view(ol, h, w)), ctypes.byref(view(op, h, w)), 0, h, 0, h, ctypes.byref(ext), 0.3, K2, K4)
+        torch.cuda.synchronize()
+        sync()
+        r = torch.equal(ol.view(torch.int64), x.view(torch.int64)) and torch.equal(op.view(torch.int64), y.view(torch.int64))
+        ok &= r
+        print(f"float64 {h}x{w} KL={kl}: {'bit-identical' if r else 'MISMATCH'}", flush=True)
+h = w = 16384
+a = torch.rand((h, w), device="cuda", generator=g, dtype=torch.float64)
+b = torch.rand((h, w), device="cuda", generator=g, dtype=torch.float64)
+a2, b2 = torch.empty_like(a), torch.empty_like(a)
+va, vb, va2, vb2 = (view(t, h, w) for t in (a, b, a2, b2))
+ext = N.box3((0, 0), (h, w))
+for kl in (4, 8):
+    torch.cuda.synchronize()
+    sync()
+    ev[0].record()
+    src, dst = (va, vb), (va2, vb2)
+    for _ in range(96 // kl):
+        N.call("cq_wave5_fused", 0, 0, N.CQ_F64, kl, ctypes.byref(src[0]), ctypes.byref(src[1]), ctypes.byref(dst[0]),
+               ctypes.byref(dst[1]), 0, h, 0, h, ctypes.byref(ext), 0.25, K2, K4)
+        src, dst = dst, src
+    ev[1].record()
+    sync()
+    ms = ev[0].elapsed_time(ev[1])
+    print(f"float64 fused KL={kl} 96 steps: {ms:.2f} ms = {24 * h * w * 96 / ms / 1e6:.0f} GB/s effective (24 B/cell/step)",
+          flush=True)
 print("ALL OK" if ok else "FAILED", flush=True)
 sys.exit(0 if ok else 1)

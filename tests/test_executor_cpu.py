@@ -329,8 +329,8 @@ def test_partially_pinned_input_is_bounced_through_a_copy(fake, monkeypatch):
 
 
 def test_fused_wave_chain_float64(fake):
-    """float64 (the reference's own kind) chains fuse too; an odd block count
-    is fixed by plain steps (no KL=8 block)."""
+    """float64 (the reference's own kind) chains fuse too, with the same
+    8/4-step block planning as float32."""
     from oracle import native as onat
     fake(1)
     h, w, steps = 160, 48, 22
@@ -338,7 +338,7 @@ def test_fused_wave_chain_float64(fake):
     prog = W.wave_program(h, w, steps=steps, kind="float64", c=0.3, u0=u0, up0=u0)
     s = E.Session(cq.generate_commands(prog.graph(), 2), E.Placement(1, 0, (0,)))
     ch = s.chains[0]
-    assert [b.kl for b in ch.blocks] == [4] * 4 and len(ch.plain) == 6
+    assert [b.kl for b in ch.blocks] == [8, 4, 4, 4] and len(ch.plain) == 2
     s.execute(upload=True)
     s.synchronize()
     res = s.results()
