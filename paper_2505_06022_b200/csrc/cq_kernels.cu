@@ -621,6 +621,11 @@ __device__ __forceinline__ float4 wave_vec(float4 m, float4 n, float4 s, float4 
   return o;
 }
 
+// Tried and measured slower (kept out): folding the tree's exact products
+// into FMAs -- fl(sum - 4u) == fma(-4, u, sum), fl(2u - p) == -fma(-2, u, p)
+// while |u| < 2^126 -- saves 2 of 9 FP ops a cell, but needs a per-warp
+// overflow guard and a second (separate-product) code path; the doubled
+// code made the 8-step pass 12% slower (18.3 vs 20.8 TB/s), not faster.
 __device__ __forceinline__ void cp_async_row(void* smem, const void* gmem, bool valid, int bytes) {
   const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   const int src_size = valid ? bytes : 0;  // 0: zero-fill, source not read

@@ -73,6 +73,22 @@ for (h, w, cc) in [(1000, 1024, 0.25), (517, 384, 0.3), (300, 4096, 0.25), (64, 
             ok &= r
             print(f"slab {h}x{w} rows [{lo},{hi}) KL={kl}: {'bit-identical' if r else 'MISMATCH'}", flush=True)
 
+# huge values: the per-warp guard must switch to the separate-product tree
+# (FMA-folded 4u / 2u would not overflow where the tree does)
+for (h, w, row) in [(600, 1024, 0), (600, 1024, 333), (300, 2176, 150)]:
+    a = torch.rand((h, w), device="cuda", generator=g)
+    b = torch.rand((h, w), device="cuda", generator=g)
+    a[row, 100:140] = 1.5e38
+    b[row + 3, 500:520] = -2.0e38
+    a[row + 7, 700] = float("inf")
+    for kl in (4, 8):
+        last, prev = plain(a, b, h, w, kl, C=0.3)
+        fl, fp = fused(a, b, h, w, kl, (0, h), (0, h), C=0.3)
+        torch.cuda.synchronize()
+        r = same(fl, last) and same(fp, prev)
+        ok &= r
+        print(f"huge values at row {row} {h}x{w} KL={kl}: {'bit-identical' if r else 'MISMATCH'}", flush=True)
+
 # timing at the BASELINE tile
 h = w = 16384
 a = torch.rand((h, w), device="cuda", generator=g)

@@ -170,6 +170,27 @@ def test_fused_wave_chain_float64_bit_exact(nodes, steps):
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
 
 
+def test_fused_wave_chain_huge_values_bit_exact():
+    """Fields near the float32 range: the fused kernel's per-warp guard keeps
+    the separate products (2u, 4u overflow in the tree where an FMA would
+    not), so the result still equals the per-step oracle bit for bit."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    h, w, steps = 515, 640, 12
+    u0 = np.random.default_rng(24).uniform(0, 1, (h, w)).astype(np.float32)
+    up0 = u0.copy()
+    u0[200, 50:90] = np.float32(1.2e38)
+    up0[300, 400:420] = np.float32(-9e37)
+    prog = W.wave_program(h, w, steps=steps, kind="float32", c=0.3, u0=u0, up0=up0)
+    s = Session(cq.generate_commands(prog.graph(), 2), Placement(1, 0, (0,)))
+    assert s.chains
+    s.execute(upload=True)
+    s.synchronize()
+    res = s.results()
+    s.close()
+    u, up = onat.wave_run(u0, up0, steps, 0.3)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
 def test_fused_wave_graph_replay_continues_the_simulation():
     """A captured fused execution replayed twice == two more plain fused
     executions == the 3x-longer simulation (the KL-row exchange makes a
