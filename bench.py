@@ -13,7 +13,7 @@ Buffer/Task/TaskGraph -> generate_commands -> B200 executor.
 * e2e       -- the public API with host buffers: ``run_batch`` of K
                simulations, each uploading its inputs from pinned host memory
                (H2D inside the timed region) and reading both result fields
-               back, two in flight so the PCIe directions and the SMs overlap;
+               back, three in flight so the PCIe directions and the SMs overlap;
                the one-at-a-time ``run(plan)`` number is reported as e2e.sync.
 * roofline  -- the dominant kernel: the temporally blocked wave pass
                (cq_wave5_fused, 8 time steps per HBM pass: 16 algorithmic
@@ -311,12 +311,14 @@ def bench_wave(args, dist, placement, peaks):
     # one-at-a-time run(plan) is reported beside it ("sync").
     gather = "root" if world == 1 else "local"
     out_box = Box((lo, 0), (hi, Wd))
+    depth = 3
     outs = [{"u": E.pinned_empty((H, Wd), np.float32, out_box),
-             "up": E.pinned_empty((H, Wd), np.float32, out_box)} for _ in range(2)]
-    E.run_batch(plan, [(None, outs[k % 2]) for k in range(max(2, args.warmup))], gather=gather)
+             "up": E.pinned_empty((H, Wd), np.float32, out_box)} for _ in range(depth)]
+    E.run_batch(plan, [(None, outs[k % depth]) for k in range(max(depth, args.warmup))], gather=gather,
+                depth=depth)
     dist.barrier()
     t0 = time.perf_counter()
-    batch = E.run_batch(plan, [(None, outs[k % 2]) for k in range(args.steps)], gather=gather)
+    batch = E.run_batch(plan, [(None, outs[k % depth]) for k in range(args.steps)], gather=gather, depth=depth)
     e2e_s = dist.max(time.perf_counter() - t0)
     e2e = 12 * cells / e2e_s / 1e9
     res_buffers = batch[-1]
@@ -345,7 +347,7 @@ def bench_wave(args, dist, placement, peaks):
         "value": value, "ms_per_step": dev_ms / args.steps, "plan_s": plan_s,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite,
-                "api": "executor.run_batch (two simulations in flight: upload, kernels and read-back overlap)",
+                "api": "executor.run_batch (three simulations in flight: upload, kernels and read-back overlap)",
                 "sync": {"value": 12 * cells / sync_s / 1e9, "ms_per_step": sync_s * 1e3 / args.steps,
                          "api": "executor.run (one simulation at a time)"}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],

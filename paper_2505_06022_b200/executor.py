@@ -1548,28 +1548,33 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
     return RunResult(buffers=buffers, trace=events, makespan=makespan, plan=plan, measured=measured)
 
 
-def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Placement] = None):
-    """Run ``plan`` once per job with two executions in flight: while one
-    simulation computes and its results travel back (device->host), the next
-    one's inputs travel in (host->device) -- the copy engines of both PCIe
-    directions and the SMs work at once.  Each job is ``(inputs, out)``:
+def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Placement] = None,
+              depth: int = 3):
+    """Run ``plan`` once per job with ``depth`` executions in flight: while
+    one simulation computes and another's results travel back (device->host),
+    the next one's inputs travel in (host->device) -- both PCIe directions and
+    the SMs work at once.  All sessions upload on one stream and read back on
+    another (each copy direction is one engine anyway); a session is reused
+    once its previous read-back is complete.  Each job is ``(inputs, out)``:
     ``inputs`` {buffer: host array} (None: the plan's own initial arrays) and
-    ``out`` {buffer: destination array} (None: fresh arrays).  Returns the list
-    of per-job buffer dicts, as ``run(...).buffers``.  Results are identical to
+    ``out`` {buffer: destination array} (None: fresh arrays; with ``out``
+    arrays, a caller reusing them must give ``depth`` sets).  Returns the list
+    of per-job buffer dicts, as ``run(...).buffers``; results are identical to
     calling ``run`` per job."""
     if gather not in ("root", "local", "none"):
         raise ValidationError(f"unknown gather mode '{gather}'")
-    sessions = [Session(plan, placement, trace=False,
-                        copy_streams=(N.STREAM_LANE0 + 2 * i, N.STREAM_LANE0 + 2 * i + 1)) for i in range(2)]
+    depth = max(1, int(depth))
+    sessions = [Session(plan, placement, trace=False, copy_streams=(N.STREAM_LANE0, N.STREAM_LANE0 + 1))
+                for _ in range(min(depth, max(1, len(jobs))))]
     if sessions[0].pl.world > 1 and gather == "root":
         for s in sessions:
             s.close()
         raise ValidationError("run_batch across ranks reads back locally: use gather='local' or 'none'")
     results = [None] * len(jobs)
-    inflight = [None, None]
+    inflight = [None] * len(sessions)
     try:
         for k, (inputs, out) in enumerate(jobs):
-            slot = k % 2
+            slot = k % len(sessions)
             s = sessions[slot]
             if inflight[slot] is not None:
                 idx, state = inflight[slot]
@@ -1582,11 +1587,11 @@ def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Pla
                 s.reset_inputs()
             s.execute(upload=True)
             inflight[slot] = (k, s.issue_results(gather, out))
-        for slot in sorted(range(2), key=lambda t: inflight[t][0] if inflight[t] else -1):
-            if inflight[slot] is not None:
-                idx, state = inflight[slot]
-                results[idx] = sessions[slot].finish_results(state)
-                sessions[slot].synchronize()
+        order = sorted((t for t in range(len(sessions)) if inflight[t] is not None), key=lambda t: inflight[t][0])
+        for slot in order:
+            idx, state = inflight[slot]
+            results[idx] = sessions[slot].finish_results(state)
+            sessions[slot].synchronize()
     finally:
         for s in sessions:
             s.close()
