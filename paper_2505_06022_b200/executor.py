@@ -1097,12 +1097,17 @@ class Session:
         and the destinations of version-1 pushes); upload=False re-runs the
         commands on the device-resident state (benchmarking)."""
         if self.t0 is None:
-            for d in self.devices:
-                ev = self.event(d, timing=True)
-                N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
-                self._t0[d] = ev
-                for s in N.SIDE_STREAMS:
-                    N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
+            if self.want_trace:
+                # the trace's time origin: every stream starts after it
+                for d in self.devices:
+                    ev = self.event(d, timing=True)
+                    N.call("cq_event_record", ctypes.c_uint64(ev), d, N.STREAM_COMPUTE)
+                    self._t0[d] = ev
+                    for s in N.SIDE_STREAMS:
+                        N.call("cq_stream_wait_event", d, s, ctypes.c_uint64(ev))
+            # untraced: no fork -- this session's ordering is its hazard
+            # events, so its uploads need not wait for other sessions'
+            # kernels on the shared compute stream (run_batch)
             self.t0 = dict(self._t0)
         self.uploading = upload
         if upload:
