@@ -13,7 +13,7 @@ Buffer/Task/TaskGraph -> generate_commands -> B200 executor.
 * e2e       -- the public API with host buffers: ``run_batch`` of K
                simulations, each uploading its inputs from pinned host memory
                (H2D inside the timed region) and reading both result fields
-               back, three in flight so the PCIe directions and the SMs overlap;
+               back, two in flight so the PCIe directions and the SMs overlap;
                the one-at-a-time ``run(plan)`` number is reported as e2e.sync.
 * roofline  -- the dominant kernel: the temporally blocked wave pass
                (cq_wave5_fused, 8 time steps per HBM pass: 16 algorithmic
@@ -311,7 +311,7 @@ def bench_wave(args, dist, placement, peaks):
     # one-at-a-time run(plan) is reported beside it ("sync").
     gather = "root" if world == 1 else "local"
     out_box = Box((lo, 0), (hi, Wd))
-    depth = 3
+    depth = int(os.environ.get("CQ_BATCH_DEPTH", "2"))
     outs = [{"u": E.pinned_empty((H, Wd), np.float32, out_box),
              "up": E.pinned_empty((H, Wd), np.float32, out_box)} for _ in range(depth)]
     E.run_batch(plan, [(None, outs[k % depth]) for k in range(max(depth, args.warmup))], gather=gather,
@@ -347,7 +347,7 @@ def bench_wave(args, dist, placement, peaks):
         "value": value, "ms_per_step": dev_ms / args.steps, "plan_s": plan_s,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite,
-                "api": "executor.run_batch (three simulations in flight: upload, kernels and read-back overlap)",
+                "api": f"executor.run_batch (depth {depth}: upload, kernels and read-back of simulations overlap)",
                 "sync": {"value": 12 * cells / sync_s / 1e9, "ms_per_step": sync_s * 1e3 / args.steps,
                          "api": "executor.run (one simulation at a time)"}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],

@@ -49,8 +49,8 @@ enum {
   CQ_STREAM_BOUNDARY = 1,
   CQ_STREAM_COMM = 2,
   CQ_STREAM_LANE0 = 3,
-  CQ_NUM_LANES = 4,
-  CQ_NUM_STREAMS = 7
+  CQ_NUM_LANES = 8,
+  CQ_NUM_STREAMS = 11
 };
 
 #define CQ_MAX_DIMS 3

@@ -18,7 +18,7 @@ CQ_OK, CQ_ERR_CUDA, CQ_ERR_NCCL, CQ_ERR_NVML, CQ_ERR_ARG = 0, 1, 2, 3, 4
 CQ_ERR_PERMISSION, CQ_ERR_UNSUPPORTED, CQ_ERR_EVAL, CQ_ERR_MAPPER = 5, 6, 7, 8
 CQ_F64, CQ_F32, CQ_I64 = 0, 1, 2
 STREAM_COMPUTE, STREAM_BOUNDARY, STREAM_COMM = 0, 1, 2
-STREAM_LANE0, NUM_LANES = 3, 4
+STREAM_LANE0, NUM_LANES = 3, 8
 ALL_STREAMS = tuple(range(STREAM_LANE0 + NUM_LANES))
 SIDE_STREAMS = ALL_STREAMS[1:]   # joined to / forked from the compute stream
 SGEMM_FFMA, SGEMM_3XTF32 = 0, 1

@@ -1554,13 +1554,12 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
 
 
 def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Placement] = None,
-              depth: int = 3):
+              depth: int = 2):
     """Run ``plan`` once per job with ``depth`` executions in flight: while
     one simulation computes and another's results travel back (device->host),
     the next one's inputs travel in (host->device) -- both PCIe directions and
-    the SMs work at once.  All sessions upload on one stream and read back on
-    another (each copy direction is one engine anyway); a session is reused
-    once its previous read-back is complete.  Each job is ``(inputs, out)``:
+    the SMs work at once.  Each session uploads and reads back on its own
+    streams; a session is reused once its previous read-back is complete.  Each job is ``(inputs, out)``:
     ``inputs`` {buffer: host array} (None: the plan's own initial arrays) and
     ``out`` {buffer: destination array} (None: fresh arrays; with ``out``
     arrays, a caller reusing them must give ``depth`` sets).  Returns the list
@@ -1568,9 +1567,12 @@ def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Pla
     calling ``run`` per job."""
     if gather not in ("root", "local", "none"):
         raise ValidationError(f"unknown gather mode '{gather}'")
-    depth = max(1, int(depth))
-    sessions = [Session(plan, placement, trace=False, copy_streams=(N.STREAM_LANE0, N.STREAM_LANE0 + 1))
-                for _ in range(min(depth, max(1, len(jobs))))]
+    depth = max(1, min(int(depth), N.NUM_LANES // 2))
+    # each session uploads and reads back on its own pair of lanes (copies of
+    # different sessions then proceed concurrently on the copy engines)
+    sessions = [Session(plan, placement, trace=False,
+                        copy_streams=(N.STREAM_LANE0 + 2 * i, N.STREAM_LANE0 + 2 * i + 1))
+                for i in range(min(depth, max(1, len(jobs))))]
     if sessions[0].pl.world > 1 and gather == "root":
         for s in sessions:
             s.close()
