@@ -13,7 +13,7 @@ Buffer/Task/TaskGraph -> generate_commands -> B200 executor.
 * e2e       -- the public API with host buffers: ``run_batch`` of K
                simulations, each uploading its inputs from pinned host memory
                (H2D inside the timed region) and reading both result fields
-               back, two in flight so the PCIe directions and the SMs overlap;
+               back, three in flight so the PCIe directions and the SMs overlap;
                the one-at-a-time ``run(plan)`` number is reported as e2e.sync.
 * roofline  -- the dominant kernel: the temporally blocked wave pass
                (cq_wave5_fused, 8 time steps per HBM pass: 16 algorithmic
@@ -311,7 +311,7 @@ def bench_wave(args, dist, placement, peaks):
     # one-at-a-time run(plan) is reported beside it ("sync").
     gather = "root" if world == 1 else "local"
     out_box = Box((lo, 0), (hi, Wd))
-    depth = int(os.environ.get("CQ_BATCH_DEPTH", "2"))
+    depth = int(os.environ.get("CQ_BATCH_DEPTH", "3"))
     outs = [{"u": E.pinned_empty((H, Wd), np.float32, out_box),
              "up": E.pinned_empty((H, Wd), np.float32, out_box)} for _ in range(depth)]
     E.run_batch(plan, [(None, outs[k % depth]) for k in range(max(depth, args.warmup))], gather=gather,

@@ -1554,7 +1554,7 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
 
 
 def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Placement] = None,
-              depth: int = 2):
+              depth: int = 3):
     """Run ``plan`` once per job with ``depth`` executions in flight: while
     one simulation computes and another's results travel back (device->host),
     the next one's inputs travel in (host->device) -- both PCIe directions and
