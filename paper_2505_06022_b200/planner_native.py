@@ -17,7 +17,7 @@ import numpy as np
 from . import _native as N
 from .energy import resolve_target, select_frequency
 from .model import AccessMode, All, Fixed, Neighborhood, OneToOne, Slice
-from .region import Region, _mk, _new, _set
+from .region import Region, _raw as _mk, _blank as _new, _put as _set
 from .scheduler import (AwaitPushCommand, Chunk, ExecuteCommand, Plan, PushCommand,
                         _resolve_devices)
 from .errors import NativeError, ValidationError
