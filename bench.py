@@ -213,7 +213,7 @@ def bench_wave(args, dist, placement, peaks):
     if sess.chains:
         ch = sess.chains[0]
         execution = (f"temporal blocking (fusion.py): {len(ch.blocks)} out-of-place passes "
-                     f"(KL = {', '.join(str(b.kl) for b in ch.blocks[-2:])} ...) of cq_wave5_fused + "
+                     f"({' + '.join(f'{sum(b.kl == k for b in ch.blocks)} x KL{k}' for k in sorted({b.kl for b in ch.blocks}, reverse=True))}) of cq_wave5_fused + "
                      f"{len(ch.plain)} one-step launches per 100 steps; KL-row halo exchange per pass "
                      f"(bit-identical to the per-step plan)")
     else:

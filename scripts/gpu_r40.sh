@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/ -q -m gpu -x > gpurun_out/gpu_tests.log 2>&1; echo "exit=$?" >> gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "exit=$?" >> gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench_r40.log 2>&1; echo "exit=$?" >> gpurun_out/bench_r40.log
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_r40.log 2>&1; echo "exit=$?" >> gpurun_out/bench_ref_r40.log
