@@ -7,6 +7,7 @@
 // contraction: explicit __*_rn intrinsics), so float64 results are
 // bit-identical to the reference and float32 results are bit-identical to a
 // binary32 restatement of the same tree.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -665,7 +666,8 @@ struct FusedShape {
 template <typename T, int KL, int V, int D, int RB>
 __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL, V>::kMinBlocks)
     wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last, cq_view_t out_prev, int64_t in_lo,
-                       int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c, T k2, T k4) {
+                       int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c, T k2, T k4,
+                       int64_t seg) {
   typedef typename FVec<T, V>::T Vec;
   static_assert(KL >= 2 && KL % V == 0, "strip offsets must stay vector aligned");
   static_assert(D % 3 == 0, "prefetch ring must be a multiple of the window");
@@ -678,9 +680,9 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   // [KL][3][32] per warp after all rings: level j's rows by slot (OLD_SM only)
   Vec* olds = reinterpret_cast<Vec*>(fused_smem) + (size_t)WPB_ * D * 2 * 32 + (size_t)warp * KL * 3 * 32;
   const int64_t strip = (int64_t)blockIdx.x * FusedShape<KL, V>::kWarps + warp;
-  const int64_t r0 = out_lo + (int64_t)blockIdx.y * RB;
+  const int64_t r0 = out_lo + (int64_t)blockIdx.y * seg;  // seg output rows per block (launch_fused)
   if (strip * SW >= W || r0 >= out_hi) return;  // warp-uniform
-  const int64_t r1 = min(r0 + (int64_t)RB, out_hi);
+  const int64_t r1 = min(r0 + seg, out_hi);
   const int64_t c0 = strip * SW - KL;  // first loaded column of the strip
   const int64_t col = c0 + lane * V;
   const bool colok = col >= 0 && col < W;
@@ -780,6 +782,38 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   cp_async_wait<0>();
 }
 
+// Rows per block.  A block marches its rows plus 2*KL halo rows, and one
+// KL = 8 block fills an SM.  A fixed segment is wrong on short slabs (a
+// node's slab at high node counts, a strong-scaled run): 512 rows x 19 strip
+// groups is 38 blocks for 148 SMs.  So pick the number of waves w and the
+// longest segment <= cap that fills them, minimising (w + 1) * (seg + 2 KL)
+// -- the extra block is the tail/imbalance of the slowest (border) block.
+// The caps (224 rows for KL = 8, 64 for KL = 4) and the tail weight come
+// from a sweep of 6 slab heights x 9 segments (profiles/r01/
+// fused_seg_sweep.log): the rule lands within 3% of the best segment on
+// average; longer segments were slower even at equal work (16384 rows,
+// KL = 8: 529 rows 1.17 ms vs 256 rows 1.04 ms).  CQ_FUSED_SEG=<rows>
+// forces a fixed segment.
+static int64_t fused_segment(int64_t rows, int64_t gx, int64_t slots, int kl, int64_t cap) {
+  const char* env = getenv("CQ_FUSED_SEG");  // read per launch (sweeps set it between launches)
+  const int64_t forced = env ? (int64_t)atoll(env) : 0;
+  if (forced > 0) return forced;
+  if (slots <= 0) return cap;
+  int64_t best = cap;
+  double best_cost = 1e300;
+  for (int64_t w = 1; w <= 64; ++w) {
+    const int64_t ny = (w * slots) / gx;
+    if (ny < 1) continue;
+    const int64_t seg = std::min(cap, std::max<int64_t>(32, (rows + ny - 1) / ny));
+    const int64_t blocks = gx * ((rows + seg - 1) / seg);
+    const int64_t waves = (blocks + slots - 1) / slots;
+    const double cost = (double)(waves + 1) * (double)(seg + 2 * kl);
+    if (cost < best_cost) best_cost = cost, best = seg;
+    if (seg == 32) break;
+  }
+  return best;
+}
+
 template <typename T, int KL, int V, int D, int RB>
 static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& upr, const cq_view_t& ol,
                         const cq_view_t& op, int64_t in_lo, int64_t in_hi, int64_t out_lo, int64_t out_hi,
@@ -787,11 +821,21 @@ static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& up
   constexpr int sw = 32 * V - 2 * KL;
   const int64_t strips = (W + sw - 1) / sw;
   constexpr int WPB = FusedShape<KL, V>::kWarps;
-  dim3 grid((unsigned)((strips + WPB - 1) / WPB), (unsigned)((out_hi - out_lo + RB - 1) / RB));
   auto kern = wave5_fused_kernel<T, KL, V, D, RB>;
   const int smem = WPB * (D * 2 + (FusedShape<KL, V>::kOldInSmem ? KL * 3 : 0)) * 32 * V * (int)sizeof(T);
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4);
+  // resident blocks per SM of this instantiation (same on every B200)
+  static const int per_sm = [&] {
+    int nb = 0;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, 32 * WPB, smem) == cudaSuccess ? nb : 0;
+  }();
+  int dev = 0, sms = 0;
+  CQ_CHECK_CUDA(cudaGetDevice(&dev));
+  CQ_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t gx = (strips + WPB - 1) / WPB, rows = out_hi - out_lo;
+  const int64_t seg = fused_segment(rows, gx, (int64_t)per_sm * sms, KL, std::min<int64_t>(RB, KL == 8 ? 224 : 64));
+  dim3 grid((unsigned)gx, (unsigned)((rows + seg - 1) / seg));
+  kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, seg);
   return CQ_OK;
 }
 
@@ -912,8 +956,9 @@ int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t
              "cq_wave5_fused: rows [%lld, %lld) are not determined by input rows [%lld, %lld)",
              (long long)out_lo, (long long)out_hi, (long long)in_lo, (long long)in_hi);
   // tuning: CQ_WAVE_FUSED_CFG="V,D,RB" (lane width, cp.async ring depth,
-  // rows per warp segment); default 4,6,128 for KL = 4 (2 blocks / SM) and
-  // 4,6,256 for KL = 8 (1 block / SM: its 8 register windows need ~200 regs)
+  // upper bound on rows per block, see fused_segment); default 4,6,128 for
+  // KL = 4 (2 blocks / SM) and 4,6,256 for KL = 8 (1 block / SM: its 8
+  // register windows need ~200 regs)
   static int cfg_env = [] {
     int v = 0, d = 0, rb = 0;
     if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d,%d", &v, &d, &rb);
