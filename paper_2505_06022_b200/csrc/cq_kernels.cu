@@ -785,20 +785,22 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
 // Rows per block.  A block marches its rows plus 2*KL halo rows, and one
 // KL = 8 block fills an SM.  A fixed segment is wrong on short slabs (a
 // node's slab at high node counts, a strong-scaled run): 512 rows x 19 strip
-// groups is 38 blocks for 148 SMs.  So pick the number of waves w and the
-// longest segment <= cap that fills them, minimising (w + 1) * (seg + 2 KL)
-// -- the extra block is the tail/imbalance of the slowest (border) block.
-// The caps (224 rows for KL = 8, 64 for KL = 4) and the tail weight come
-// from a sweep of 6 slab heights x 9 segments (profiles/r01/
-// fused_seg_sweep.log): the rule lands within 3% of the best segment on
-// average; longer segments were slower even at equal work (16384 rows,
-// KL = 8: 529 rows 1.17 ms vs 256 rows 1.04 ms).  CQ_FUSED_SEG=<rows>
-// forces a fixed segment.
+// groups of 256 rows is 38 blocks for 148 SMs.  Rule, from a sweep of 6
+// slab heights x 9 segments (profiles/r01/fused_seg_sweep.log, seg_check.log):
+// * tall slabs (>= 4 waves of blocks at the cap): the cap, 224 rows for
+//   KL = 8 (longer segments measured slower even at equal work: 16384 rows,
+//   529 rows 1.17 ms vs 224 rows 1.03 ms);
+// * otherwise pick the number of waves w and the longest segment <= cap that
+//   fills them, minimising (w + 1/4) * (seg + 2 KL) (the quarter block is the
+//   tail of the slowest, border block): 512 rows run in 0.059 ms instead of
+//   0.168 ms;
+// * KL = 4 (two blocks per SM) was fastest at 32 rows at every height.
+// CQ_FUSED_SEG=<rows> forces a fixed segment.
 static int64_t fused_segment(int64_t rows, int64_t gx, int64_t slots, int kl, int64_t cap) {
   const char* env = getenv("CQ_FUSED_SEG");  // read per launch (sweeps set it between launches)
   const int64_t forced = env ? (int64_t)atoll(env) : 0;
   if (forced > 0) return forced;
-  if (slots <= 0) return cap;
+  if (slots <= 0 || gx * ((rows + cap - 1) / cap) >= 4 * slots) return cap;
   int64_t best = cap;
   double best_cost = 1e300;
   for (int64_t w = 1; w <= 64; ++w) {
@@ -807,7 +809,7 @@ static int64_t fused_segment(int64_t rows, int64_t gx, int64_t slots, int kl, in
     const int64_t seg = std::min(cap, std::max<int64_t>(32, (rows + ny - 1) / ny));
     const int64_t blocks = gx * ((rows + seg - 1) / seg);
     const int64_t waves = (blocks + slots - 1) / slots;
-    const double cost = (double)(waves + 1) * (double)(seg + 2 * kl);
+    const double cost = ((double)waves + 0.25) * (double)(seg + 2 * kl);
     if (cost < best_cost) best_cost = cost, best = seg;
     if (seg == 32) break;
   }
@@ -833,7 +835,7 @@ static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& up
   CQ_CHECK_CUDA(cudaGetDevice(&dev));
   CQ_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int64_t gx = (strips + WPB - 1) / WPB, rows = out_hi - out_lo;
-  const int64_t seg = fused_segment(rows, gx, (int64_t)per_sm * sms, KL, std::min<int64_t>(RB, KL == 8 ? 224 : 64));
+  const int64_t seg = fused_segment(rows, gx, (int64_t)per_sm * sms, KL, std::min<int64_t>(RB, KL == 8 ? 224 : 32));
   dim3 grid((unsigned)gx, (unsigned)((rows + seg - 1) / seg));
   kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, seg);
   return CQ_OK;
