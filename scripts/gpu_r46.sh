@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+# plain runs first (ncu only after the same command exits 0)
+timeout 300 python scripts/fused_prof.py 8 > gpurun_out/fused_prof_r46.log 2>&1 || exit 1
+timeout 300 python scripts/fused_prof.py 4 >> gpurun_out/fused_prof_r46.log 2>&1 || exit 1
+timeout 900 python bench.py --steps 2 --warmup 3 --no-cpu --no-energy --no-kernels > gpurun_out/bench_small_r46.log 2>&1 || exit 1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:wave5_fused -s 1 -c 1 -o gpurun_out/fused8_r46 python scripts/fused_prof.py 8 > gpurun_out/ncu_fused8_r46.log 2>&1; echo "exit=$?" >> gpurun_out/ncu_fused8_r46.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:wave5_fused -s 1 -c 1 -o gpurun_out/fused4_r46 python scripts/fused_prof.py 4 > gpurun_out/ncu_fused4_r46.log 2>&1; echo "exit=$?" >> gpurun_out/ncu_fused4_r46.log
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r46.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-energy --no-kernels > gpurun_out/ncu_list_r46.log 2>&1; echo "exit=$?" >> gpurun_out/ncu_list_r46.log
