@@ -90,6 +90,9 @@ int cq_free(int device, void* ptr);
 int cq_pool_trim(int device);
 int cq_host_register(void* ptr, int64_t bytes);
 int cq_host_unregister(void* ptr);
+/* Page-locked host memory owned by libcq (small staging buffers). */
+int cq_host_alloc(int64_t bytes, void** ptr);
+int cq_host_free(void* ptr);
 
 /* Copies -- the Push/AwaitPush payload move (simulator.py:166-193) and the
  * final gather (simulator.py:210-222). Box copies are 2-D/3-D strided DMA
@@ -213,6 +216,11 @@ int cq_jit_launch(uint64_t handle, int device, int stream, const cq_expr_t* expr
 /* Sticky per-device error flag written by cq_expr_eval: code 0 / CQ_ERR_EVAL /
  * CQ_ERR_MAPPER with the first failing cell (row-major minimum). */
 int cq_error_flag(int device, int* code, int64_t point[CQ_MAX_DIMS], int clear);
+/* The same flag copied asynchronously on `stream` into 32 bytes of page-locked
+ * host memory (cq_host_alloc): {key, point[3]}, key ~0 = no error, else the
+ * low 4 bits are the code.  Lets a pipelined caller check a run without a
+ * blocking read that would queue behind other runs' transfers. */
+int cq_error_flag_async(int device, int stream, void* host32);
 
 /* All-pairs N-body kick: for i in [i_lo, i_hi): v_i += dt * sum_j m_j d_ij /
  * (|d_ij|^2 + eps2)^(3/2), d_ij = p_j - p_i; pos holds all n bodies (float4

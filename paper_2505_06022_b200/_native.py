@@ -68,6 +68,8 @@ _SIGS = {
     "cq_free": (i32, [i32, vp]),
     "cq_pool_trim": (i32, [i32]),
     "cq_host_register": (i32, [vp, i64]),
+    "cq_host_alloc": (i32, [i64, P(vp)]),
+    "cq_host_free": (i32, [vp]),
     "cq_host_unregister": (i32, [vp]),
     "cq_copy_h2d": (i32, [i32, i32, vp, vp, i64]),
     "cq_copy_d2h": (i32, [i32, i32, vp, vp, i64]),
@@ -106,6 +108,7 @@ _SIGS = {
                              P(CqBox), ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     "cq_expr_eval": (i32, [i32, i32, P(CqExpr)]),
     "cq_error_flag": (i32, [i32, P(i32), P(i64), i32]),
+    "cq_error_flag_async": (i32, [i32, i32, vp]),
     "cq_nbody_kick": (i32, [i32, i32, vp, i64, vp, vp, i64, i64, ctypes.c_float, ctypes.c_float]),
     "cq_nbody_drift": (i32, [i32, i32, vp, vp, vp, i64, ctypes.c_float]),
     "cq_sgemm": (i32, [i32, i32, i32, vp, i64, vp, i64, vp, i64, i64, i64, i64]),

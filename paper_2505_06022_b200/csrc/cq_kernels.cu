@@ -1037,6 +1037,13 @@ int cq_error_flag(int device, int* code, int64_t point[CQ_MAX_DIMS], int clear) 
   return CQ_OK;
 }
 
+int cq_error_flag_async(int device, int stream, void* host32) {
+  CQ_GET_STREAM(device, stream);
+  CQ_REQUIRE(host32 != nullptr, "cq_error_flag_async: null host buffer");
+  CQ_CHECK_CUDA(cudaMemcpyAsync(host32, ds->error_flag, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+  return CQ_OK;
+}
+
 int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const float* vel_in,
                   float* vel, int64_t i_lo, int64_t i_hi, float eps2, float dt) {
   CQ_GET_STREAM(device, stream);

@@ -230,6 +230,17 @@ int cq_pool_trim(int device) {
   return CQ_OK;
 }
 
+int cq_host_alloc(int64_t bytes, void** ptr) {
+  CQ_REQUIRE(bytes > 0 && ptr != nullptr, "cq_host_alloc: bad arguments");
+  CQ_CHECK_CUDA(cudaMallocHost(ptr, (size_t)bytes));
+  return CQ_OK;
+}
+
+int cq_host_free(void* ptr) {
+  if (ptr) CQ_CHECK_CUDA(cudaFreeHost(ptr));
+  return CQ_OK;
+}
+
 int cq_host_register(void* ptr, int64_t bytes) {
   cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
   if (e == cudaErrorHostMemoryAlreadyRegistered) {

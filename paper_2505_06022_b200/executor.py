@@ -213,6 +213,14 @@ def _pin_state(start, end):
     return "free"
 
 
+def _raise_flag(code, point):
+    """The reference's exception for a device error-flag code."""
+    if code == N.CQ_ERR_EVAL:
+        raise EvalError(f"integer division by zero at id {point}")
+    if code == N.CQ_ERR_MAPPER:
+        raise MapperViolationError(f"read at id {point} outside the mapped region")
+
+
 def _pin_span(arr: np.ndarray, box=None, keep=True):
     """Page-lock the bytes of a large ``arr`` spanning ``box`` (whole array if
     None); a rank of a weak-scaled run pins only its own rows of a big host
@@ -418,6 +426,7 @@ class Session:
         self.graph_events = []
         self.host_init = {}
         self._overridden = set()
+        self._flag_host = None   # page-locked copies of the devices' error flags (run_batch)
         self._sched = None
         self._raw = None        # the plan's schedule before fusion (schedule())
         self._lanes = None      # node -> compute stream (lane())
@@ -1234,6 +1243,9 @@ class Session:
     def close(self):
         self._drop_graph()
         self.release()
+        if self._flag_host is not None:
+            N.call("cq_host_free", self._flag_host)
+            self._flag_host = None
         for pool in self.free_events.values():
             for ev in pool:
                 N.call("cq_event_destroy", ctypes.c_uint64(ev))
@@ -1250,10 +1262,28 @@ class Session:
             code = ctypes.c_int32()
             pt = (ctypes.c_int64 * 3)()
             N.call("cq_error_flag", d, ctypes.byref(code), pt, 1)
-            if code.value == N.CQ_ERR_EVAL:
-                raise EvalError(f"integer division by zero at id {tuple(pt)}")
-            if code.value == N.CQ_ERR_MAPPER:
-                raise MapperViolationError(f"read at id {tuple(pt)} outside the mapped region")
+            _raise_flag(code.value, tuple(pt))
+
+    def _post_error_flags(self):
+        """Queue a copy of every device's error flag behind the read-back
+        (``finish_results`` decodes it): a blocking read would wait for the
+        copy engines, i.e. for the transfers of other runs in flight."""
+        if self._flag_host is None:
+            ptr = ctypes.c_void_p()
+            N.call("cq_host_alloc", 32 * len(self.devices), ctypes.byref(ptr))
+            self._flag_host = ptr
+        base = self._flag_host.value
+        for k, d in enumerate(self.devices):
+            N.call("cq_error_flag_async", d, self.d2h_stream, ctypes.c_void_p(base + 32 * k))
+
+    def _check_posted_flags(self):
+        words = (ctypes.c_uint64 * (4 * len(self.devices))).from_address(self._flag_host.value)
+        for k, d in enumerate(self.devices):
+            key = words[4 * k]
+            if key != 0xFFFFFFFFFFFFFFFF:
+                pt = tuple(ctypes.c_int64(words[4 * k + j]).value for j in (1, 2, 3))
+                N.call("cq_error_flag", d, ctypes.byref(ctypes.c_int32()), (ctypes.c_int64 * 3)(), 1)  # clear
+                _raise_flag(int(key & 15), pt)
 
     # ---- gather ------------------------------------------------------------
     def results(self, gather: str = "root", out: Optional[dict] = None):
@@ -1276,6 +1306,7 @@ class Session:
                         ev = self.event(d)
                         N.call("cq_event_record", ctypes.c_uint64(ev), d, st)
                         N.call("cq_stream_wait_event", d, self.d2h_stream, ctypes.c_uint64(ev))
+            self._post_error_flags()
         out = {}
         root = self.pl.rank == 0
         pending = []
@@ -1326,18 +1357,19 @@ class Session:
             if span is not None:
                 temp_pins.append(span)
         bounced = []
+        deferred = []   # pieces bound for pageable host memory
         st = self.d2h_stream
         for view, arr, region in direct:
             ha = N.box3((0,) * arr.ndim, arr.shape)
             for box in region.boxes:
-                cb = _cbox(box)
-                if _needs_bounce(arr, box):
-                    tmp = np.empty(box.shape, dtype=arr.dtype)
-                    bounced.append((arr, box, tmp))
-                    N.call("cq_copy_box_d2h", view.device, st, view.itemsize,
-                           ctypes.c_void_p(tmp.ctypes.data), ctypes.byref(cb), ctypes.byref(view.c),
-                           ctypes.byref(cb))
+                # a DMA into pageable memory blocks the host until the stream
+                # reaches it (here: the end of the whole run), so such pieces
+                # -- e.g. the halo rows a rank also holds, outside its pinned
+                # output rows -- are copied by finish_results instead
+                if _pin_state(*_byte_span(arr, box)) != "pinned":
+                    deferred.append((view, arr, box))
                     continue
+                cb = _cbox(box)
                 N.call("cq_copy_box_d2h", view.device, st, view.itemsize,
                        ctypes.c_void_p(arr.ctypes.data), ctypes.byref(ha), ctypes.byref(view.c),
                        ctypes.byref(cb))
@@ -1346,15 +1378,35 @@ class Session:
             if st != N.STREAM_COMM:
                 raise ValidationError("gather='root' across ranks reads back on the comm stream")
             self.gather_remote(remote, bounced)
-        return (out, bounced, temp_pins, root)
+        return (out, bounced, temp_pins, root, deferred, join)
 
     def finish_results(self, state):
         """Wait for ``issue_results``' copies and return the buffers."""
         if state is None:
             return {}
-        out, bounced, temp_pins, root = state
+        out, bounced, temp_pins, root, deferred, posted = state
         for d in self.devices:
             N.call("cq_stream_synchronize", d, self.d2h_stream)
+        if posted:
+            self._check_posted_flags()
+        st = self.d2h_stream
+        for view, arr, box in deferred:
+            # the run is complete: pageable copies no longer wait on anything;
+            # one straddling a registration edge goes through a temporary
+            cb = _cbox(box)
+            if _needs_bounce(arr, box):
+                tmp = np.empty(box.shape, dtype=arr.dtype)
+                bounced.append((arr, box, tmp))
+                N.call("cq_copy_box_d2h", view.device, st, view.itemsize,
+                       ctypes.c_void_p(tmp.ctypes.data), ctypes.byref(cb), ctypes.byref(view.c),
+                       ctypes.byref(cb))
+            else:
+                N.call("cq_copy_box_d2h", view.device, st, view.itemsize,
+                       ctypes.c_void_p(arr.ctypes.data), ctypes.byref(N.box3((0,) * arr.ndim, arr.shape)),
+                       ctypes.byref(view.c), ctypes.byref(cb))
+        if deferred:
+            for d in self.devices:
+                N.call("cq_stream_synchronize", d, st)
         for arr, box, tmp in bounced:
             arr[tuple(slice(lo, hi) for lo, hi in zip(box.mins, box.maxs))] = tmp
         for span in temp_pins:
@@ -1579,26 +1631,49 @@ def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Pla
         raise ValidationError("run_batch across ranks reads back locally: use gather='local' or 'none'")
     results = [None] * len(jobs)
     inflight = [None] * len(sessions)
+    # uploads (and read-backs) of consecutive runs are chained in job order:
+    # sharing the link between all runs in flight would delay the first
+    # run's kernels until every queued upload is done
+    chain = {}
+
+    def follow(s, stream, key):
+        for d in s.devices:
+            if (key, d) in chain:
+                N.call("cq_stream_wait_event", d, stream, ctypes.c_uint64(chain[(key, d)]))
+
+    def mark(s, stream, key):
+        for d in s.devices:
+            ev = s.event(d)
+            N.call("cq_event_record", ctypes.c_uint64(ev), d, stream)
+            chain[(key, d)] = ev
+
     try:
         for k, (inputs, out) in enumerate(jobs):
             slot = k % len(sessions)
             s = sessions[slot]
             if inflight[slot] is not None:
                 idx, state = inflight[slot]
-                results[idx] = s.finish_results(state)
-                s.check_errors()
+                results[idx] = s.finish_results(state)   # also checks the run's error flags
+                if state is None:
+                    s.check_errors()
                 s.recycle()
             if inputs:
                 s.set_inputs(inputs)
             elif s._overridden:
                 s.reset_inputs()
+            follow(s, s.h2d_stream, "up")
             s.execute(upload=True)
+            mark(s, s.h2d_stream, "up")
+            follow(s, s.d2h_stream, "down")
             inflight[slot] = (k, s.issue_results(gather, out))
+            mark(s, s.d2h_stream, "down")
         order = sorted((t for t in range(len(sessions)) if inflight[t] is not None), key=lambda t: inflight[t][0])
         for slot in order:
             idx, state = inflight[slot]
             results[idx] = sessions[slot].finish_results(state)
             sessions[slot].synchronize()
+            if state is None:
+                sessions[slot].check_errors()
     finally:
         for s in sessions:
             s.close()

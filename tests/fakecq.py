@@ -373,6 +373,23 @@ class FakeLib:
         self.launches.append("jit")
         return self.cq_expr_eval(d, s, X)
 
+    def cq_host_alloc(self, nbytes, p):
+        buf = np.zeros(int(_val(nbytes)), dtype=np.uint8)
+        self.host_bufs = getattr(self, "host_bufs", {})
+        self.host_bufs[buf.ctypes.data] = buf
+        _obj(p).value = buf.ctypes.data
+        return 0
+
+    def cq_host_free(self, p):
+        getattr(self, "host_bufs", {}).pop(_val(p), None)
+        return 0
+
+    def cq_error_flag_async(self, d, s, host):
+        words = (ctypes.c_uint64 * 4).from_address(_val(host))
+        words[0] = 0xFFFFFFFFFFFFFFFF if not self.flag else self.flag
+        words[1] = words[2] = words[3] = 0
+        return 0
+
     def cq_error_flag(self, d, code, pt, clear):
         _obj(code).value = self.flag or 0
         if clear:

@@ -347,6 +347,20 @@ def test_fused_wave_chain_float64(fake):
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
 
 
+def test_run_batch_raises_posted_error_flag(fake):
+    """run_batch reads each run's error flag from a copy posted behind its
+    read-back and raises the reference's exception, also for the last runs
+    (which are only drained, never recycled)."""
+    lib = fake(1)
+    prog = W.saxpy_program(64, kind="float32")
+    plan = cq.generate_commands(prog.graph(), 2)
+    lib.flag = N.CQ_ERR_EVAL
+    with pytest.raises(cq.EvalError):
+        E.run_batch(plan, [(None, None)] * 2, placement=E.Placement(1, 0, (0,)))
+    lib.flag = None
+    assert len(E.run_batch(plan, [(None, None)] * 3, placement=E.Placement(1, 0, (0,)))) == 3
+
+
 def test_run_batch_matches_run(fake):
     """run_batch (two sessions in flight, their own upload / read-back
     streams) returns, per job, exactly what run() returns -- including jobs

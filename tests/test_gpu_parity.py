@@ -10,6 +10,7 @@ import pytest
 
 import paper_2505_06022_b200 as cq
 from paper_2505_06022_b200 import lowering, workloads as W
+from paper_2505_06022_b200 import executor as E
 from paper_2505_06022_b200.executor import run
 from oracle import dsl
 from oracle import native as onat
@@ -278,6 +279,25 @@ def test_integer_division_by_zero_raises_eval_error():
     t = cq.Task("div", ext, [cq.Accessor("a", cq.AccessMode.READ), cq.Accessor("b", cq.AccessMode.WRITE)], body)
     with pytest.raises(cq.EvalError):
         _run_program(bufs, [t], 2)
+
+
+@pytest.mark.parametrize("jobs", [1, 4])
+def test_run_batch_reports_eval_error(jobs):
+    """run_batch checks each run's error flag from a copy queued behind its
+    read-back (no blocking read); the error surfaces for the last run too."""
+    ext = cq.Box.from_shape((16,))
+    bufs = {"a": cq.Buffer("a", ext, "int64", cq.BufferInit.iota()),
+            "b": cq.Buffer("b", ext, "int64", cq.BufferInit.zeros())}
+    body = {"b": cq.parse_kernel("7 / (a[i] - 5)", {"a": 1}, set(), 1)}
+    t = cq.Task("div", ext, [cq.Accessor("a", cq.AccessMode.READ), cq.Accessor("b", cq.AccessMode.WRITE)], body)
+    g = cq.TaskGraph(bufs)
+    g.submit(t)
+    plan = cq.generate_commands(g, 2)
+    with pytest.raises(cq.EvalError):
+        E.run_batch(plan, [(None, None)] * jobs, depth=2)
+    # the flag was cleared: a clean program runs afterwards
+    prog = W.saxpy_program(4099, kind="float32")
+    E.run_batch(cq.generate_commands(prog.graph(), 2), [(None, None)] * 2)
 
 
 def test_mapper_violation_raises():
