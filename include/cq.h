@@ -174,6 +174,17 @@ int cq_wave5(int device, int stream, int kind, const cq_view_t* u, const cq_view
 int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t* u, const cq_view_t* upr,
                    const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
                    int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4);
+/* The same pass with a magnitude bound: amax_in (device float, or NULL)
+ * bounds |X(t)|, |X(t-1)| over the rows this launch reads; when it is below
+ * 2^124 / (3 + 8|c|)^levels the interior blocks use an FMA form of the body
+ * that is bit-identical while nothing overflows (7 instead of 9 FP
+ * operations per cell).  amax_out (device float, or NULL) receives, by
+ * atomic max, max |value| over the rows written -- the next pass's amax_in.
+ * cq_wave5_fused == this with both NULL. */
+int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const cq_view_t* u, const cq_view_t* upr,
+                           const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
+                           int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4,
+                           const float* amax_in, float* amax_out);
 
 /* Device interpreter for arbitrary task bodies (eval_kernel, kernel.py:291-331
  * with ReadView clamping + mapper check, model.py:442-453). */

@@ -106,6 +106,9 @@ _SIGS = {
                        ctypes.c_double, ctypes.c_double, ctypes.c_double]),
     "cq_wave5_fused": (i32, [i32, i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqView), i64, i64, i64, i64,
                              P(CqBox), ctypes.c_double, ctypes.c_double, ctypes.c_double]),
+    "cq_wave5_fused_bounded": (i32, [i32, i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqView), i64, i64,
+                                     i64, i64, P(CqBox), ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                     vp, vp]),
     "cq_expr_eval": (i32, [i32, i32, P(CqExpr)]),
     "cq_error_flag": (i32, [i32, P(i32), P(i64), i32]),
     "cq_error_flag_async": (i32, [i32, i32, vp]),

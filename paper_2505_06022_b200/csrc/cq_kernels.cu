@@ -8,6 +8,7 @@
 // bit-identical to the reference and float32 results are bit-identical to a
 // binary32 restatement of the same tree.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -622,11 +623,53 @@ __device__ __forceinline__ float4 wave_vec(float4 m, float4 n, float4 s, float4 
   return o;
 }
 
-// Tried and measured slower (kept out): folding the tree's exact products
-// into FMAs -- fl(sum - 4u) == fma(-4, u, sum), fl(2u - p) == -fma(-2, u, p)
-// while |u| < 2^126 -- saves 2 of 9 FP ops a cell, but needs a per-warp
-// overflow guard and a second (separate-product) code path; the doubled
-// code made the 8-step pass 12% slower (18.3 vs 20.8 TB/s), not faster.
+// Fast form of the same tree for fields known to be bounded: while 4u and
+// 2u do not overflow (|u| < 2^125), fl(4u) and fl(2u) are exact, so
+//   fl(sum - fl(4u)) == fma(-4, u, sum)        (one rounding of the same value)
+//   fl(fl(2u) - p)   == -fma(-2, u, p)         (RN is sign-symmetric)
+//   fl(t + fl(c*lap)) == fl(fl(c*lap) - fma(-2, u, p))
+// -- bit-identical, 7 instead of 9 FP-pipe operations per cell.  The bound
+// comes from the previous pass (wave5_fused_kernel's amax_out); the first
+// pass of a chain, fields that grow past the limit and the border path use
+// the exact form.  (A per-warp guard inside the loop measured slower: 18.3 vs
+// 20.8 TB/s; the decision here is one load per block.)
+__device__ __forceinline__ float4 wave_vec_fast(float4 m, float4 n, float4 s, float4 p, float wv, float ev,
+                                                float c) {
+  const f32x2 nsA = add2(pack2(n.x, n.y), pack2(s.x, s.y));
+  const f32x2 nsB = add2(pack2(n.z, n.w), pack2(s.z, s.w));
+  float a0, a1, b0, b1;
+  unpack2(nsA, a0, a1);
+  unpack2(nsB, b0, b1);
+  a0 = __fadd_rn(__fadd_rn(a0, wv), m.y);
+  a1 = __fadd_rn(__fadd_rn(a1, m.x), m.z);
+  b0 = __fadd_rn(__fadd_rn(b0, m.y), m.w);
+  b1 = __fadd_rn(__fadd_rn(b1, m.z), ev);
+  const f32x2 uA = pack2(m.x, m.y), uB = pack2(m.z, m.w);
+  const f32x2 m4 = pack2(-4.f, -4.f), m2 = pack2(-2.f, -2.f);
+  const f32x2 lapA = fma2(uA, m4, pack2(a0, a1)), lapB = fma2(uB, m4, pack2(b0, b1));
+  const f32x2 fA = fma2(uA, m2, pack2(p.x, p.y)), fB = fma2(uB, m2, pack2(p.z, p.w));
+  float l0, l1, l2, l3, f0, f1, f2, f3;
+  unpack2(lapA, l0, l1);
+  unpack2(lapB, l2, l3);
+  unpack2(fA, f0, f1);
+  unpack2(fB, f2, f3);
+  float4 o;
+  o.x = __fsub_rn(__fmul_rn(c, l0), f0);
+  o.y = __fsub_rn(__fmul_rn(c, l1), f1);
+  o.z = __fsub_rn(__fmul_rn(c, l2), f2);
+  o.w = __fsub_rn(__fmul_rn(c, l3), f3);
+  return o;
+}
+template <typename Vec>
+__device__ __forceinline__ Vec wave_vec_fast(Vec m, Vec n, Vec s, Vec p, decltype(m.x) wv, decltype(m.x) ev,
+                                            decltype(m.x) c) {
+  return wave_vec(m, n, s, p, wv, ev, c);  // other widths / float64: exact form
+}
+
+__device__ __forceinline__ float abs_max(float4 v) { return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))); }
+__device__ __forceinline__ float abs_max(float2 v) { return fmaxf(fabsf(v.x), fabsf(v.y)); }
+__device__ __forceinline__ float abs_max(double2 v) { return (float)fmax(fabs(v.x), fabs(v.y)); }
+
 __device__ __forceinline__ void cp_async_row(void* smem, const void* gmem, bool valid, int bytes) {
   const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   const int src_size = valid ? bytes : 0;  // 0: zero-fill, source not read
@@ -667,7 +710,7 @@ template <typename T, int KL, int V, int D, int RB>
 __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL, V>::kMinBlocks)
     wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last, cq_view_t out_prev, int64_t in_lo,
                        int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c, T k2, T k4,
-                       int64_t seg) {
+                       int64_t seg, const float* __restrict__ amax_in, float* __restrict__ amax_out, float limit) {
   typedef typename FVec<T, V>::T Vec;
   static_assert(KL >= 2 && KL % V == 0, "strip offsets must stay vector aligned");
   static_assert(D % 3 == 0, "prefetch ring must be a multiple of the window");
@@ -698,6 +741,10 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   const int64_t bc0 = (int64_t)blockIdx.x * WPB * SW - KL;  // first loaded column of the block
   const bool interior = bc0 > 0 && bc0 + (WPB - 1) * SW + 32 * V < W && rb - KL > 0 && re < H && rb >= in_lo &&
                         re <= in_hi;
+  // |inputs| bound from the previous pass (amax_in, null: unknown); NaN
+  // compares false and keeps the exact form
+  const bool fast = interior && amax_in != nullptr && *amax_in < limit;
+  float amax = 0.f;  // max |stored value| of this warp (amax_out)
   const int64_t us = u.stride[1], ps = upr.stride[1];
   const T* ub = (const T*)u.ptr + (colok ? col : 0) - u.alloc.lo[2] + (rb - u.alloc.lo[1]) * us;
   const T* pb = (const T*)upr.ptr + (colok ? col : 0) - upr.alloc.lo[2] + (rb - upr.alloc.lo[1]) * ps;
@@ -705,8 +752,9 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   T* sp = (T*)out_prev.ptr + (col - out_prev.alloc.lo[2]) + (r0 - out_prev.alloc.lo[1]) * out_prev.stride[1];
   const int64_t ls = out_last.stride[1], pstr = out_prev.stride[1];
 
-  auto march = [&](auto edge_tag) {
+  auto march = [&](auto edge_tag, auto fast_tag) {
     constexpr bool EDGE = decltype(edge_tag)::value;
+    constexpr bool FAST = decltype(fast_tag)::value;
     // fetch input row r (offset k rows from rb) into ring slot `slot`
     auto fetch = [&](int slot, int64_t r, int64_t k) {
       bool ok = true;
@@ -750,17 +798,23 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
           if (col + V == W) ev = last_of(mid);
         }
         const Vec pp = (j == 1) ? P[sm] : old_of(j >= 2 ? j - 2 : 0);
-        const Vec o = wave_vec(mid, nn, ss, pp, wv, ev, c);
+        const Vec o = FAST ? wave_vec_fast(mid, nn, ss, pp, wv, ev, c) : wave_vec(mid, nn, ss, pp, wv, ev, c);
         if (j < KL) {
           L[j][s] = o;
           if (OLD_SM) olds[(j * 3 + s) * 32 + lane] = o;
         }
         if (j == KL - 1 && rho >= r0 && rho < r1) {
-          if (keep) __stcs(reinterpret_cast<Vec*>(sp), o);
+          if (keep) {
+            __stcs(reinterpret_cast<Vec*>(sp), o);
+            amax = fmaxf(amax, abs_max(o));
+          }
           sp += pstr;
         }
         if (j == KL && rho >= r0) {
-          if (keep) __stcs(reinterpret_cast<Vec*>(sl), o);
+          if (keep) {
+            __stcs(reinterpret_cast<Vec*>(sl), o);
+            amax = fmaxf(amax, abs_max(o));
+          }
           sl += ls;
         }
       }
@@ -777,9 +831,16 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
     for (int sd = 0; sd < D; ++sd)
       if (base + sd < re) row(base + sd, sd);
   };
-  if (interior) march(std::false_type{});
-  else march(std::true_type{});
+  if (fast) march(std::false_type{}, std::true_type{});
+  else if (interior) march(std::false_type{}, std::false_type{});
+  else march(std::true_type{}, std::false_type{});
   cp_async_wait<0>();
+  if (amax_out != nullptr) {
+    // values are >= 0, so their int bit patterns order like the floats
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) atomicMax(reinterpret_cast<int*>(amax_out), __float_as_int(amax));
+  }
 }
 
 // Rows per block.  A block marches its rows plus 2*KL halo rows, and one
@@ -819,7 +880,8 @@ static int64_t fused_segment(int64_t rows, int64_t gx, int64_t slots, int kl, in
 template <typename T, int KL, int V, int D, int RB>
 static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& upr, const cq_view_t& ol,
                         const cq_view_t& op, int64_t in_lo, int64_t in_hi, int64_t out_lo, int64_t out_hi,
-                        int64_t H, int64_t W, T c, T k2, T k4) {
+                        int64_t H, int64_t W, T c, T k2, T k4, const float* amax_in, float* amax_out,
+                        float limit) {
   constexpr int sw = 32 * V - 2 * KL;
   const int64_t strips = (W + sw - 1) / sw;
   constexpr int WPB = FusedShape<KL, V>::kWarps;
@@ -837,7 +899,8 @@ static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& up
   const int64_t gx = (strips + WPB - 1) / WPB, rows = out_hi - out_lo;
   const int64_t seg = fused_segment(rows, gx, (int64_t)per_sm * sms, KL, std::min<int64_t>(RB, KL == 8 ? 224 : 32));
   dim3 grid((unsigned)gx, (unsigned)((rows + seg - 1) / seg));
-  kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, seg);
+  kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, seg, amax_in,
+                                     amax_out, limit);
   return CQ_OK;
 }
 
@@ -937,6 +1000,14 @@ int cq_wave5(int device, int stream, int kind, const cq_view_t* u, const cq_view
 int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t* u, const cq_view_t* upr,
                    const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
                    int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4) {
+  return cq_wave5_fused_bounded(device, stream, kind, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo,
+                                out_hi, extent, c, k2, k4, nullptr, nullptr);
+}
+
+int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const cq_view_t* u, const cq_view_t* upr,
+                           const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
+                           int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4,
+                           const float* amax_in, float* amax_out) {
   CQ_GET_STREAM(device, stream);
   if (out_hi <= out_lo) return CQ_OK;
   const int64_t H = extent->hi[1], W = extent->hi[2];
@@ -967,16 +1038,25 @@ int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t
     return v ? v * 10000 + d * 1000 + rb : 0;
   }();
   const int cfg = cfg_env ? cfg_env : (levels == 8 ? 4 * 10000 + 6 * 1000 + 256 : 4 * 10000 + 6 * 1000 + 128);
+  // the fast form is exact while every value of the pass stays below 2^125
+  // (then 2u and 4u do not overflow); one step grows max|X| by at most
+  // g = 3 + 8|c| (|2u| + |p| + |c| |n+s+w+e-4u|), so inputs below
+  // 2^124 / g^levels are safe (CQ_WAVE_FAST=0 disables the fast form)
+  static const bool fast_ok = [] {
+    const char* e = getenv("CQ_WAVE_FAST");
+    return !(e && e[0] == '0');
+  }();
+  const float limit = fast_ok ? (float)(std::ldexp(1.0, 124) / std::pow(3.0 + 8.0 * std::fabs(c) + 1e-3, levels)) : 0.f;
   int status;
   if (kind == CQ_F64) {
     // two doubles per lane (16-byte rows): 56 (KL = 4) or 48 (KL = 8) valid
     // columns per warp strip
     if (levels == 4)
       status = launch_fused<double, 4, 2, 6, 128>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi,
-                                                  H, W, c, k2, k4);
+                                                  H, W, c, k2, k4, amax_in, amax_out, limit);
     else
       status = launch_fused<double, 8, 2, 6, 256>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi,
-                                                  H, W, c, k2, k4);
+                                                  H, W, c, k2, k4, amax_in, amax_out, limit);
     if (status != CQ_OK) return status;
     CQ_CHECK_LAUNCH();
     return CQ_OK;
@@ -985,7 +1065,7 @@ int cq_wave5_fused(int device, int stream, int kind, int levels, const cq_view_t
 #define CQ_FUSED_CASE(VV, DD, RBB, KL)                                                               \
   case (VV * 10000 + DD * 1000 + RBB) * 10 + KL:                                                   \
     status = launch_fused<float, KL, VV, DD, RBB>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, \
-                                                  H, W, (float)c, (float)k2, (float)k4);                       \
+                                                  H, W, (float)c, (float)k2, (float)k4, amax_in, amax_out, limit); \
     break;
     CQ_FUSED_CASE(4, 6, 128, 4) CQ_FUSED_CASE(4, 6, 128, 8)
     CQ_FUSED_CASE(4, 6, 256, 4) CQ_FUSED_CASE(4, 6, 256, 8)

@@ -566,6 +566,25 @@ class Session:
             self.views[(node, buf)] = _View(node, self.dev(node), buf, bb, b.itemsize)
             if (node, buf) in fused:
                 self.alt[(node, buf)] = _View(node, self.dev(node), buf, bb, b.itemsize)
+        # per float32 chain and local node: one device float per block
+        # boundary, max |X| over the node's rows after that block (written by
+        # the block's launches, read by the next: cq_wave5_fused_bounded).
+        # Zeroed once; later runs only raise them, which keeps them bounds.
+        self._amax = {}
+        for ci, ch in enumerate(self.chains):
+            if self.buffers[ch.a].element_kind != "float32":
+                continue
+            for node in sorted(ch.rows):
+                if not self.local(node):
+                    continue
+                dev, n = self.dev(node), len(ch.blocks) + 1
+                p = ctypes.c_void_p()
+                N.call("cq_malloc", dev, 4 * n, ctypes.byref(p))
+                zero = np.zeros(n, np.float32)
+                N.call("cq_copy_h2d", dev, N.STREAM_COMPUTE, p, ctypes.c_void_p(zero.ctypes.data), 4 * n)
+                N.call("cq_stream_synchronize", dev, N.STREAM_COMPUTE)
+                self.scratch.append((dev, p.value))
+                self._amax[(ci, node)] = p.value
 
     # ---- host-initialised data -----------------------------------------
     def host_array(self, buf):
@@ -819,6 +838,8 @@ class Session:
                         break
         ext = _cbox(b.extent)
         W = ch.W
+        ci = self.chains.index(ch)
+        bi = ch.blocks.index(block)
         if self._exec_of is None:
             self._exec_of = {(c.task_id, c.node): c for c in self.plan.commands if isinstance(c, ExecuteCommand)}
         for node in sorted(ch.rows):
@@ -829,8 +850,15 @@ class Session:
             oa, ob = self.alt[(node, ch.a)], self.alt[(node, ch.b)]
             marks = []
             interior, edge_t, edge_b = fusion.node_ranges(ch, node, kl)
+            slots = self._amax.get((ci, node))
+            # the interior reads only the node's own rows, all written by the
+            # previous block's launches (ordered before it by those rows'
+            # hazards), so the previous block's bound applies; the edges read
+            # received halo rows and stay on the exact form
+            amax_out = None if slots is None else slots + 4 * (bi + 1)
             for rng, stream in ((interior, self.lane(node)), (edge_t, N.STREAM_BOUNDARY),
                                 (edge_b, N.STREAM_BOUNDARY)):
+                amax_in = slots + 4 * bi if (slots is not None and bi > 0 and rng is interior) else None
                 if rng is None or rng[3] <= rng[2]:
                     continue
                 in_lo, in_hi, out_lo, out_hi = rng
@@ -838,12 +866,12 @@ class Session:
                 rout = Region.from_box(Box((out_lo, 0), (out_hi, W)))
                 acc = [(ua, rin, False), (pb, rin, False), (oa, rout, True), (ob, rout, True)]
 
-                def go(stream=stream, rng=rng):
-                    N.call("cq_wave5_fused", dev, stream, N.KIND_CODE[b.element_kind], kl, ctypes.byref(ua.c),
-                           ctypes.byref(pb.c),
+                def go(stream=stream, rng=rng, amax_in=amax_in):
+                    N.call("cq_wave5_fused_bounded", dev, stream, N.KIND_CODE[b.element_kind], kl,
+                           ctypes.byref(ua.c), ctypes.byref(pb.c),
                            ctypes.byref(oa.c), ctypes.byref(ob.c), rng[0], rng[1], rng[2], rng[3],
                            ctypes.byref(ext), ctypes.c_double(ch.c), ctypes.c_double(ch.k2),
-                           ctypes.c_double(ch.k4))
+                           ctypes.c_double(ch.k4), ctypes.c_void_p(amax_in), ctypes.c_void_p(amax_out))
                 t = self.issue(dev, stream, acc, go)
                 marks.append(t)
                 if self.want_trace:

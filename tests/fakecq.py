@@ -269,6 +269,14 @@ class FakeLib:
         self.launches.append("wave5")
         return 0
 
+    def cq_wave5_fused_bounded(self, d, s, kind, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi,
+                               ext, c, k2, k4, amax_in, amax_out):
+        # the bound only selects an equivalent arithmetic form on the GPU
+        self.fused_bounds = getattr(self, "fused_bounds", [])
+        self.fused_bounds.append((_val(amax_in), _val(amax_out)))
+        return self.cq_wave5_fused(d, s, kind, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi,
+                                   ext, c, k2, k4)
+
     def cq_wave5_fused(self, d, s, kind, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi, ext, c,
                        k2, k4):
         """KL ping-pong steps on rows [in_lo, in_hi) (edge rows replicate,

@@ -273,6 +273,36 @@ def test_fused_wave_chain_matches_oracle(fake, monkeypatch, steps, nodes, ndev):
     assert sum(1 for e in trace if e.kind == "push") == n_push
 
 
+def test_fused_chain_magnitude_bounds_wiring(fake):
+    """Every fused launch of a float32 chain writes its node's bound slot for
+    the block; only interior launches after the first block read the
+    previous block's slot (edges read received rows: exact form)."""
+    lib = fake(1)
+    h, w = 200, 64
+    u0 = np.random.default_rng(13).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=24, kind="float32", u0=u0, up0=u0)
+    plan = cq.generate_commands(prog.graph(), 2)
+    s = E.Session(plan, E.Placement(1, 0, (0,)))
+    ch = s.chains[0]
+    s.execute(upload=True)
+    s.synchronize()
+    s.close()
+    slots = {node: s._amax[(0, node)] for node in ch.rows}
+    bounds = lib.fused_bounds
+    # per block: node 0 (interior + bottom edge), node 1 (top edge + interior)
+    per_block = len(bounds) // len(ch.blocks)
+    assert per_block * len(ch.blocks) == len(bounds) == 4 * len(ch.blocks)
+    for bi in range(len(ch.blocks)):
+        launches = bounds[bi * per_block:(bi + 1) * per_block]
+        outs = {o for _i, o in launches}
+        assert outs == {slots[n] + 4 * (bi + 1) for n in slots}
+        reads = [i for i, _o in launches if i]
+        if bi == 0:
+            assert reads == []
+        else:
+            assert sorted(reads) == sorted(slots[n] + 4 * bi for n in slots)
+
+
 def test_fused_chain_disabled_and_graph_replay(fake, monkeypatch):
     from oracle import native as onat
     lib = fake(1)

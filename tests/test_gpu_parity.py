@@ -172,9 +172,10 @@ def test_fused_wave_chain_float64_bit_exact(nodes, steps):
 
 
 def test_fused_wave_chain_huge_values_bit_exact():
-    """Fields near the float32 range: the fused kernel's per-warp guard keeps
-    the separate products (2u, 4u overflow in the tree where an FMA would
-    not), so the result still equals the per-step oracle bit for bit."""
+    """Fields near the float32 range: the passes' magnitude bound is above
+    the limit, so the fused kernel keeps the separate products (2u, 4u
+    overflow in the tree where an FMA would not), and the result still equals
+    the per-step oracle bit for bit."""
     from paper_2505_06022_b200.executor import Placement, Session
     h, w, steps = 515, 640, 12
     u0 = np.random.default_rng(24).uniform(0, 1, (h, w)).astype(np.float32)
@@ -190,6 +191,28 @@ def test_fused_wave_chain_huge_values_bit_exact():
     s.close()
     u, up = onat.wave_run(u0, up0, steps, 0.3)
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
+@pytest.mark.parametrize("scale,c", [(1e30, 0.3), (1e-30, 0.25), (1.0, 0.45)])
+def test_fused_wave_chain_fast_form_bit_exact(scale, c):
+    """Blocks after the first take the FMA form of the body when the previous
+    block's magnitude bound allows it (cq_wave5_fused_bounded); large, tiny
+    and ordinary fields over many blocks stay bit-identical to the oracle."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    h, w, steps = 515, 640, 64
+    rng = np.random.default_rng(31)
+    u0 = (rng.uniform(-1, 1, (h, w)) * scale).astype(np.float32)
+    up0 = (rng.uniform(-1, 1, (h, w)) * scale).astype(np.float32)
+    for nodes in (1, 3):
+        prog = W.wave_program(h, w, steps=steps, kind="float32", c=c, u0=u0, up0=up0)
+        s = Session(cq.generate_commands(prog.graph(), nodes), Placement(1, 0, (0,)))
+        assert s.chains and len(s.chains[0].blocks) >= 6
+        s.execute(upload=True)
+        s.synchronize()
+        res = s.results()
+        s.close()
+        u, up = onat.wave_run(u0, up0, steps, c)
+        assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up), (scale, c, nodes)
 
 
 def test_fused_wave_graph_replay_continues_the_simulation():
