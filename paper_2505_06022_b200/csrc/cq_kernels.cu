@@ -564,7 +564,9 @@ __device__ __forceinline__ float last_of(float4 v) { return v.w; }
 // with .rn and --fmad=false), which would skip a rounding of the DSL tree.
 // So no packed product ever feeds a packed add: the body's k2 = 2 and k4 = 4
 // products are formed as exact sums (u+u == fl(2u), 2u+2u == fl(4u), also
-// for subnormals and overflow), and c*lap is two scalar __fmul_rn.
+// for subnormals and overflow), and c*lap is two scalar __fmul_rn (float2
+// path) or a packed mul whose halves feed scalar adds, which ptxas leaves
+// alone (float4 path; the SASS of the fused kernels has no scalar FFMA).
 __device__ __forceinline__ f32x2 wave_pair(f32x2 u, f32x2 n, f32x2 s, f32x2 w, f32x2 e, f32x2 p, float c) {
   const f32x2 u2 = add2(u, u), u4 = add2(u2, u2);
   const f32x2 lap = sub2(add2(add2(add2(n, s), w), e), u4);
@@ -608,18 +610,20 @@ __device__ __forceinline__ float4 wave_vec(float4 m, float4 n, float4 s, float4 
   const f32x2 u2A = add2(uA, uA), u2B = add2(uB, uB);
   const f32x2 lapA = sub2(pack2(a0, a1), add2(u2A, u2A));
   const f32x2 lapB = sub2(pack2(b0, b1), add2(u2B, u2B));
-  float l0, l1, l2, l3;
-  unpack2(lapA, l0, l1);
-  unpack2(lapB, l2, l3);
   const f32x2 tA = sub2(u2A, pack2(p.x, p.y)), tB = sub2(u2B, pack2(p.z, p.w));
+  // c*lap packed, added as scalars (not contracted: see wave_vec_fast)
+  const f32x2 cc = pack2(c, c);
+  float l0, l1, l2, l3;
+  unpack2(mul2(cc, lapA), l0, l1);
+  unpack2(mul2(cc, lapB), l2, l3);
   float t0, t1, t2, t3;
   unpack2(tA, t0, t1);
   unpack2(tB, t2, t3);
   float4 o;
-  o.x = __fadd_rn(t0, __fmul_rn(c, l0));
-  o.y = __fadd_rn(t1, __fmul_rn(c, l1));
-  o.z = __fadd_rn(t2, __fmul_rn(c, l2));
-  o.w = __fadd_rn(t3, __fmul_rn(c, l3));
+  o.x = __fadd_rn(t0, l0);
+  o.y = __fadd_rn(t1, l1);
+  o.z = __fadd_rn(t2, l2);
+  o.w = __fadd_rn(t3, l3);
   return o;
 }
 
@@ -648,16 +652,20 @@ __device__ __forceinline__ float4 wave_vec_fast(float4 m, float4 n, float4 s, fl
   const f32x2 m4 = pack2(-4.f, -4.f), m2 = pack2(-2.f, -2.f);
   const f32x2 lapA = fma2(uA, m4, pack2(a0, a1)), lapB = fma2(uB, m4, pack2(b0, b1));
   const f32x2 fA = fma2(uA, m2, pack2(p.x, p.y)), fB = fma2(uB, m2, pack2(p.z, p.w));
+  // c*lap packed; its unpacked halves feed scalar subtractions, which ptxas
+  // does not contract (checked in the SASS: no scalar FFMA in this kernel)
+  const f32x2 cc = pack2(c, c);
+  const f32x2 clA = mul2(cc, lapA), clB = mul2(cc, lapB);
   float l0, l1, l2, l3, f0, f1, f2, f3;
-  unpack2(lapA, l0, l1);
-  unpack2(lapB, l2, l3);
+  unpack2(clA, l0, l1);
+  unpack2(clB, l2, l3);
   unpack2(fA, f0, f1);
   unpack2(fB, f2, f3);
   float4 o;
-  o.x = __fsub_rn(__fmul_rn(c, l0), f0);
-  o.y = __fsub_rn(__fmul_rn(c, l1), f1);
-  o.z = __fsub_rn(__fmul_rn(c, l2), f2);
-  o.w = __fsub_rn(__fmul_rn(c, l3), f3);
+  o.x = __fsub_rn(l0, f0);
+  o.y = __fsub_rn(l1, f1);
+  o.z = __fsub_rn(l2, f2);
+  o.w = __fsub_rn(l3, f3);
   return o;
 }
 template <typename Vec>

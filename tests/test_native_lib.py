@@ -50,3 +50,25 @@ def test_sm100a_code_in_library():
                          capture_output=True, text=True)
     assert out.returncode == 0
     assert "sm_100a" in out.stdout
+
+
+def test_wave_kernels_have_no_contracted_fma():
+    """The DSL rounds every operator, so the float32 wave kernels must not
+    contain a scalar FFMA (ptxas contracts a packed mul feeding a packed add
+    into FFMA2 even with --fmad=false; the kernels are written so it cannot).
+    The fused kernels' FFMA2 are the deliberate, exact FMA form."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    lib = os.path.join(ROOT, "paper_2505_06022_b200", "libcq.so")
+    sass = subprocess.run([tool, "-sass", lib], capture_output=True, text=True, check=True).stdout
+    funcs = re.split(r"\n\s*Function : ", sass)
+    wave = [f for f in funcs if re.match(r"_ZN2cq\d+wave5_\w*kernelIf", f)]
+    assert len(wave) >= 4
+    for f in wave:
+        name = f.split("\n", 1)[0].strip()
+        assert not re.search(r"\bFFMA\b(?!2)", f), name
+        if "fused" not in name:
+            assert "FFMA2" not in f, name
