@@ -213,6 +213,16 @@ def _pin_state(start, end):
     return "free"
 
 
+def _free_scratch(items):
+    """Free (device, pointer | _View) temporaries and empty the list."""
+    for dev, item in items:
+        if isinstance(item, _View):
+            item.free()
+        else:
+            N.call("cq_free", dev, ctypes.c_void_p(item))
+    items.clear()
+
+
 def _raise_flag(code, point):
     """The reference's exception for a device error-flag code."""
     if code == N.CQ_ERR_EVAL:
@@ -413,7 +423,9 @@ class Session:
         self.local_nodes = [n for n in range(self.nodes) if placement.is_local(n, self.nodes)]
         self.devices = sorted({placement.device_of(n, self.nodes) for n in self.local_nodes})
         self.views = {}
-        self.scratch = []
+        self.scratch = []         # this run's temporaries (freed by recycle)
+        self._graph_scratch = []  # temporaries a captured graph uses (freed with it)
+        self._slots = []          # session-lifetime device words (fused-chain bounds)
         self.events = []
         self.free_events = {}
         self.haz = _Hazards()
@@ -583,7 +595,7 @@ class Session:
                 zero = np.zeros(n, np.float32)
                 N.call("cq_copy_h2d", dev, N.STREAM_COMPUTE, p, ctypes.c_void_p(zero.ctypes.data), 4 * n)
                 N.call("cq_stream_synchronize", dev, N.STREAM_COMPUTE)
-                self.scratch.append((dev, p.value))
+                self._slots.append((dev, p.value))
                 self._amax[(ci, node)] = p.value
 
     # ---- host-initialised data -----------------------------------------
@@ -1193,6 +1205,8 @@ class Session:
         N.call("cq_graph_end", d, ctypes.byref(handle))
         self.want_trace = saved
         self._drop_graph()
+        # pack/unpack temporaries allocated while capturing belong to the graph
+        self._graph_scratch, self.scratch = self.scratch, []
         log = list(self.launch_log)
         if timed:
             # the graph's event-record nodes own these events: keep them out
@@ -1214,6 +1228,7 @@ class Session:
             N.call("cq_event_destroy", ctypes.c_uint64(ev))
         self.graph_events = []
         self.graph_log = []
+        _free_scratch(self._graph_scratch)
 
     def replay(self, times: int = 1):
         """Launch the captured graph ``times`` times (asynchronous)."""
@@ -1258,7 +1273,9 @@ class Session:
         return out
 
     def recycle(self):
-        """After a synchronize: forget hazards, recycle events and traces."""
+        """After a synchronize: forget hazards, recycle events and traces,
+        free the run's temporaries."""
+        _free_scratch(self.scratch)
         self.haz = _Hazards()
         for dev, timing, ev in self.events:
             self.free_events.setdefault((dev, timing), []).append(ev)
@@ -1555,11 +1572,9 @@ class Session:
         for v in list(self.views.values()) + list(self.alt.values()):
             v.free()
         self.alt.clear()
-        for dev, item in self.scratch:
-            if isinstance(item, _View):
-                item.free()
-            else:
-                N.call("cq_free", dev, ctypes.c_void_p(item))
+        _free_scratch(self.scratch)
+        _free_scratch(self._graph_scratch)
+        _free_scratch(self._slots)
         for dev, timing, ev in self.events:
             N.call("cq_event_destroy", ctypes.c_uint64(ev))
         self.views.clear()
@@ -1682,7 +1697,8 @@ def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Pla
             if inflight[slot] is not None:
                 idx, state = inflight[slot]
                 results[idx] = s.finish_results(state)   # also checks the run's error flags
-                if state is None:
+                if state is None:   # gather="none": nothing was joined or read back
+                    s.synchronize()
                     s.check_errors()
                 s.recycle()
             if inputs:

@@ -377,6 +377,35 @@ def test_fused_wave_chain_float64(fake):
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
 
 
+def test_run_temporaries_are_freed_by_recycle(fake):
+    """An in-place stencil (a read at a non-zero offset of the buffer the
+    task writes) snapshots its read region into a run temporary; repeated
+    runs of one session free them at recycle instead of accumulating."""
+    lib = fake(1)
+    ext = cq.Box.from_shape((64,))
+    bufs = {"a": cq.Buffer("a", ext, "float32", cq.BufferInit.iota())}
+    body = {"a": cq.parse_kernel("ar[i-1] + ar[i+1]", {"ar": 1}, set(), 1)}
+    t = cq.Task("relax", ext, [cq.Accessor("a", cq.AccessMode.READ, cq.Neighborhood((1,)), name="ar"),
+                               cq.Accessor("a", cq.AccessMode.WRITE)], body)
+    g = cq.TaskGraph(bufs)
+    g.submit(t)
+    s = E.Session(cq.generate_commands(g, 1), E.Placement(1, 0, (0,)))
+    live = []
+    for _ in range(4):
+        s.execute(upload=True)
+        s.synchronize()
+        res = s.results()
+        assert s.scratch   # the snapshot
+        s.recycle()
+        assert not s.scratch
+        live.append(len(lib.blocks))
+    s.close()
+    a = np.arange(64, dtype=np.float32)
+    want = np.concatenate([[a[0] + a[1]], a[:-2] + a[2:], [a[-2] + a[-1]]]).astype(np.float32)
+    assert dsl.same_bits(res["a"], want)
+    assert live[1] == live[-1], live
+
+
 def test_run_batch_raises_posted_error_flag(fake):
     """run_batch reads each run's error flag from a copy posted behind its
     read-back and raises the reference's exception, also for the last runs
