@@ -567,6 +567,8 @@ __device__ __forceinline__ float last_of(float4 v) { return v.w; }
 // for subnormals and overflow), and c*lap is two scalar __fmul_rn (float2
 // path) or a packed mul whose halves feed scalar adds, which ptxas leaves
 // alone (float4 path; the SASS of the fused kernels has no scalar FFMA).
+// (Forming the product as fma(c, x, -0) to keep the final add packed does
+// not work: ptxas drops the -0 addend and contracts again.)
 __device__ __forceinline__ f32x2 wave_pair(f32x2 u, f32x2 n, f32x2 s, f32x2 w, f32x2 e, f32x2 p, float c) {
   const f32x2 u2 = add2(u, u), u4 = add2(u2, u2);
   const f32x2 lap = sub2(add2(add2(add2(n, s), w), e), u4);
