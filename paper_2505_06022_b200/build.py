@@ -22,6 +22,21 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v
          "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 
 
+def _nccl_rpath():
+    """Directories searched for libnccl.so.2 at run time.  The NCCL that
+    PyTorch ships (nvidia-nccl wheel) comes first, so libcq and torch share
+    one NCCL whichever of them is loaded first (two different libnccl.so.2
+    in one process break the later one); the system copy is the fallback."""
+    import importlib.util
+    dirs = []
+    spec = importlib.util.find_spec("nvidia.nccl")
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        lib = os.path.join(base, "lib")
+        if os.path.exists(os.path.join(lib, "libnccl.so.2")):
+            dirs.append(lib)
+    return dirs + ["/usr/lib/x86_64-linux-gnu", "/usr/local/cuda/lib64"]
+
+
 def _stale(target, deps):
     if not os.path.exists(target):
         return True
@@ -63,7 +78,7 @@ def build(force=False, verbose=False) -> str:
     objs = [os.path.join(OBJ, s + ".o") for s in SOURCES]
     if force or jobs or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl", "-lnvrtc", "-ldl",
-               "-Xlinker", "-rpath,/usr/lib/x86_64-linux-gnu:/usr/local/cuda/lib64"]
+               "-Xlinker", "-rpath," + ":".join(_nccl_rpath())]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

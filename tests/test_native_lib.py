@@ -72,3 +72,42 @@ def test_wave_kernels_have_no_contracted_fma():
         assert not re.search(r"\bFFMA\b(?!2)", f), name
         if "fused" not in name:
             assert "FFMA2" not in f, name
+
+
+def test_no_cpu_fallback_without_the_library(monkeypatch):
+    """The executor never computes on the CPU: without libcq.so a run raises
+    (NativeError, a ClusterqError) instead of falling back."""
+    import paper_2505_06022_b200 as cq
+    from paper_2505_06022_b200 import workloads as W
+    monkeypatch.setattr(N, "LIB_PATH", os.path.join(ROOT, "no-such-dir", "libcq.so"))
+    monkeypatch.setattr(N, "_lib", None)
+    from paper_2505_06022_b200.scheduler import generate_commands_py
+    prog = W.saxpy_program(1024, kind="float32")
+    plan = generate_commands_py(prog.graph(), 2)
+    with pytest.raises(cq.NativeError, match="no CPU fallback"):
+        cq.run(plan)
+
+
+def test_no_cpu_fallback_without_a_gpu():
+    """With the library but no GPU (this container), a run fails loudly."""
+    if os.path.exists("/dev/nvidiactl"):
+        pytest.skip("a GPU is present")
+    import paper_2505_06022_b200 as cq
+    from paper_2505_06022_b200 import workloads as W
+    prog = W.saxpy_program(1024, kind="float32")
+    with pytest.raises(cq.ClusterqError):
+        cq.run(cq.generate_commands(prog.graph(), 1))
+
+
+def test_torch_imports_after_libcq():
+    """libcq and PyTorch share one libnccl.so.2 (the runpath prefers the NCCL
+    wheel torch uses), so importing torch after libcq is loaded works."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2505_06022_b200 import _native as N\n"
+            "N.load()\n"
+            "import torch\n"
+            "print('ok')\n") % ROOT
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
