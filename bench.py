@@ -364,7 +364,7 @@ def bench_wave(args, dist, placement, peaks):
                      "note": ("temporal blocking: one launch advances 8 time steps while reading X(t), X(t-1) "
                               "and writing two levels (16 B/cell, ncu traffic above), so the algorithmic "
                               "12 B/cell/step rate exceeds the HBM peak; the pass itself is FP32-pipe / issue "
-                              "limited (ncu, FMA form: FMA pipe 62% active, issue 71% busy, "
+                              "limited (ncu, FMA form, 12 warps/SM: FMA pipe 67% active, issue 70% busy, "
                               "profiles/r01/wave5_fused8_ncu_full_summary.txt)")
                              if dom_kind == "wave5_fused8" else None,
                      "launch_timing": timing_source},

@@ -698,10 +698,12 @@ __device__ __forceinline__ void cp_async_wait() {
 // (cp.async, one commit group per row, each lane fetches and later reads
 // back only its own V columns), so D rows of both inputs are in flight per
 // warp without holding them in registers.
-// 8 warps per block; the register-heavy KL = 8, V = 4 variant (~200
-// registers per thread) runs one block per SM -- more warps would cap it at
-// 168 registers (3 warps per SM sub-partition) and spill, which measured
-// slower (profiles/r01/fused_cfg_sweep.log).
+// The register-heavy KL = 8, V = 4 variant runs one 12-warp block per SM:
+// with 32-bit row counters and running prefetch pointers it needs ~153
+// registers, under the 168 that 3 warps per SM sub-partition allow (the
+// earlier 64-bit row arithmetic needed ~200 and capped it at 8 warps;
+// 12 warps then spilled, profiles/r01/fused_cfg_sweep.log).  Other shapes
+// run 8-warp blocks.
 template <int KL, int V>
 struct FusedShape {
   // kOldInSmem keeps the rows two iterations old of every level in shared
@@ -712,7 +714,7 @@ struct FusedShape {
   // warps gain), so the register-only variant runs one 8-warp block per SM
   // (~200 registers).
   static constexpr bool kOldInSmem = false;
-  static constexpr int kWarps = 8;
+  static constexpr int kWarps = (KL == 8 && V == 4) ? 12 : 8;
   static constexpr int kMinBlocks = KL == 8 ? 1 : 2;
 };
 
@@ -747,6 +749,8 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   // readable.  Border strips / segments take the checked path.
   // Decided per block (from blockIdx and parameters only), so the branch is
   // CTA-uniform and the shuffles inside need no divergence fallback.
+  // (Per-warp decisions with warps walking (strip, segment) pairs on a 1-D
+  // grid -- no partial block columns -- measured 2% slower.)
   constexpr int WPB = FusedShape<KL, V>::kWarps;
   const int64_t bc0 = (int64_t)blockIdx.x * WPB * SW - KL;  // first loaded column of the block
   const bool interior = bc0 > 0 && bc0 + (WPB - 1) * SW + 32 * V < W && rb - KL > 0 && re < H && rb >= in_lo &&
@@ -762,46 +766,57 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   T* sp = (T*)out_prev.ptr + (col - out_prev.alloc.lo[2]) + (r0 - out_prev.alloc.lo[1]) * out_prev.stride[1];
   const int64_t ls = out_last.stride[1], pstr = out_prev.stride[1];
 
+  // rows are counted from rb in 32-bit (t = ri - rb); the store windows in
+  // t: out_prev (level KL-1, row rb + t - KL + 1 in [r0, r1)) and out_last
+  // (level KL, row rb + t - KL >= r0; always < r1)
+  const int nrow = (int)(re - rb);
+  const int prev_lo = 2 * KL - 1, prev_hi = (int)(r1 - rb) + KL - 1, last_lo = 2 * KL;
+
   auto march = [&](auto edge_tag, auto fast_tag) {
     constexpr bool EDGE = decltype(edge_tag)::value;
     constexpr bool FAST = decltype(fast_tag)::value;
-    // fetch input row r (offset k rows from rb) into ring slot `slot`
-    auto fetch = [&](int slot, int64_t r, int64_t k) {
+    // running source pointers of the next row to prefetch (row rb + t + D)
+    const T* uf = ub + (int64_t)D * us;
+    const T* pf = pb + (int64_t)D * ps;
+    // fetch input row rb + k into ring slot `slot` from (uk, pk)
+    auto fetch = [&](int slot, int k, const T* uk, const T* pk) {
       bool ok = true;
-      int64_t kk = k;
       if (EDGE) {
+        const int64_t r = rb + k;
         ok = colok && r >= in_lo && r < in_hi;
-        if (!ok) kk = 0;  // any mapped address; zero-filled, not read
+        if (!ok) uk = ub, pk = pb;  // any mapped address; zero-filled, not read
       }
-      cp_async_row(ring + (slot * 2 + 0) * 32 + lane, ub + kk * us, ok, sizeof(Vec));
-      cp_async_row(ring + (slot * 2 + 1) * 32 + lane, pb + kk * ps, ok, sizeof(Vec));
+      cp_async_row(ring + (slot * 2 + 0) * 32 + lane, uk, ok, sizeof(Vec));
+      cp_async_row(ring + (slot * 2 + 1) * 32 + lane, pk, ok, sizeof(Vec));
     };
-    Vec L[KL][3];  // level j (0 = X(t)) rows, slot = (row - rb) % 3
+    Vec L[KL][3];  // level j (0 = X(t)) rows, slot = t % 3
     Vec P[3];      // X(t-1) rows, same slots
 #pragma unroll
     for (int q = 0; q < D; ++q) {
-      if (rb + q < re) fetch(q, rb + q, q);
+      if (q < nrow) fetch(q, q, ub + (int64_t)q * us, pb + (int64_t)q * ps);
       cp_async_commit();
     }
-    // one input row: land it, prefetch row ri + D, advance every level
-    auto row = [&](const int64_t ri, const int sd) {
-      const int s = sd % 3, so = (sd + 1) % 3, sm = (sd + 2) % 3;  // rows ri, ri-2, ri-1
-      cp_async_wait<D - 1>();  // row ri (the oldest group) has landed
+    // one input row: land it, prefetch row t + D, advance every level
+    auto row = [&](const int t, const int sd) {
+      const int s = sd % 3, so = (sd + 1) % 3, sm = (sd + 2) % 3;  // rows t, t-2, t-1
+      cp_async_wait<D - 1>();  // row t (the oldest group) has landed
       L[0][s] = ring[(sd * 2 + 0) * 32 + lane];
       P[s] = ring[(sd * 2 + 1) * 32 + lane];
       if (OLD_SM) olds[(0 * 3 + s) * 32 + lane] = L[0][s];
-      if (ri + D < re) fetch(sd, ri + D, ri + D - rb);
+      if (t + D < nrow) fetch(sd, t + D, uf, pf);
       cp_async_commit();
+      uf += us;
+      pf += ps;
       // the row two iterations old of level k (north of level k+1, u_prev of k+2)
       auto old_of = [&](int k) -> Vec { return OLD_SM ? olds[(k * 3 + so) * 32 + lane] : L[k][so]; };
 #pragma unroll
       for (int j = 1; j <= KL; ++j) {
-        const int64_t rho = ri - j;
         const Vec mid = L[j - 1][sm];
         Vec nn = old_of(j - 1), ss = L[j - 1][s];
         T wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
         T ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
         if (EDGE) {
+          const int64_t rho = rb + t - j;
           if (rho == 0) nn = mid;
           if (rho == H - 1) ss = mid;
           if (col == 0) wv = first_of(mid);
@@ -813,14 +828,14 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
           L[j][s] = o;
           if (OLD_SM) olds[(j * 3 + s) * 32 + lane] = o;
         }
-        if (j == KL - 1 && rho >= r0 && rho < r1) {
+        if (j == KL - 1 && t >= prev_lo && t < prev_hi) {
           if (keep) {
             __stcs(reinterpret_cast<Vec*>(sp), o);
             amax = fmaxf(amax, abs_max(o));
           }
           sp += pstr;
         }
-        if (j == KL && rho >= r0) {
+        if (j == KL && t >= last_lo) {
           if (keep) {
             __stcs(reinterpret_cast<Vec*>(sl), o);
             amax = fmaxf(amax, abs_max(o));
@@ -831,15 +846,15 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
     };
     // whole ring turns without a bounds test (the warp stays converged, so
     // the shuffles need no collective fallback), then the remainder
-    int64_t base = rb;
+    int base = 0;
 #pragma unroll 1
-    for (; base + D <= re; base += D) {
+    for (; base + D <= nrow; base += D) {
 #pragma unroll
       for (int sd = 0; sd < D; ++sd) row(base + sd, sd);
     }
 #pragma unroll
     for (int sd = 0; sd < D; ++sd)
-      if (base + sd < re) row(base + sd, sd);
+      if (base + sd < nrow) row(base + sd, sd);
   };
   if (fast) march(std::false_type{}, std::true_type{});
   else if (interior) march(std::false_type{}, std::false_type{});
@@ -871,15 +886,15 @@ static int64_t fused_segment(int64_t rows, int64_t gx, int64_t slots, int kl, in
   const char* env = getenv("CQ_FUSED_SEG");  // read per launch (sweeps set it between launches)
   const int64_t forced = env ? (int64_t)atoll(env) : 0;
   if (forced > 0) return forced;
-  if (slots <= 0 || gx * ((rows + cap - 1) / cap) >= 4 * slots) return cap;
+  auto blocks_for = [&](int64_t seg) { return gx * ((rows + seg - 1) / seg); };
+  if (slots <= 0 || blocks_for(cap) >= 4 * slots) return cap;
   int64_t best = cap;
   double best_cost = 1e300;
   for (int64_t w = 1; w <= 64; ++w) {
     const int64_t ny = (w * slots) / gx;
     if (ny < 1) continue;
     const int64_t seg = std::min(cap, std::max<int64_t>(32, (rows + ny - 1) / ny));
-    const int64_t blocks = gx * ((rows + seg - 1) / seg);
-    const int64_t waves = (blocks + slots - 1) / slots;
+    const int64_t waves = (blocks_for(seg) + slots - 1) / slots;
     const double cost = ((double)waves + 0.25) * (double)(seg + 2 * kl);
     if (cost < best_cost) best_cost = cost, best = seg;
     if (seg == 32) break;
