@@ -631,9 +631,12 @@ __device__ __forceinline__ float4 wave_vec(float4 m, float4 n, float4 s, float4 
 
 // Fast form of the same tree for fields known to be bounded: while 4u and
 // 2u do not overflow (|u| < 2^125), fl(4u) and fl(2u) are exact, so
-//   fl(sum - fl(4u)) == fma(-4, u, sum)        (one rounding of the same value)
-//   fl(fl(2u) - p)   == -fma(-2, u, p)         (RN is sign-symmetric)
-//   fl(t + fl(c*lap)) == fl(fl(c*lap) - fma(-2, u, p))
+//   fl(sum - fl(4u)) == fma(-4, u, sum)        (one rounding of the same sum)
+//   fl(fl(2u) - p)   == fma(2, u, -p)          (likewise)
+// with the same signed zero on exact cancellation, since an FMA's zero sum
+// follows the rules of addition.  (The sign-symmetric -fma(-2, u, p) is
+// equal only for non-zero results: it turns t = +0 into -0, and +0 + (-0)
+// differs from -0 - (+0) when c*lap is -0.)
 // -- bit-identical, 7 instead of 9 FP-pipe operations per cell.  The bound
 // comes from the previous pass (wave5_fused_kernel's amax_out); the first
 // pass of a chain, fields that grow past the limit and the border path use
@@ -651,23 +654,25 @@ __device__ __forceinline__ float4 wave_vec_fast(float4 m, float4 n, float4 s, fl
   b0 = __fadd_rn(__fadd_rn(b0, m.y), m.w);
   b1 = __fadd_rn(__fadd_rn(b1, m.z), ev);
   const f32x2 uA = pack2(m.x, m.y), uB = pack2(m.z, m.w);
-  const f32x2 m4 = pack2(-4.f, -4.f), m2 = pack2(-2.f, -2.f);
+  const f32x2 m4 = pack2(-4.f, -4.f), two = pack2(2.f, 2.f);
   const f32x2 lapA = fma2(uA, m4, pack2(a0, a1)), lapB = fma2(uB, m4, pack2(b0, b1));
-  const f32x2 fA = fma2(uA, m2, pack2(p.x, p.y)), fB = fma2(uB, m2, pack2(p.z, p.w));
-  // c*lap packed; its unpacked halves feed scalar subtractions, which ptxas
-  // does not contract (checked in the SASS: no scalar FFMA in this kernel)
+  // t = fma(2, u, -p): the same addends as fl(2u) + (-p), so also the same
+  // signed zero when 2u == p (the form -fma(-2, u, p) gives -0 there)
+  const f32x2 tA = fma2(uA, two, pack2(-p.x, -p.y)), tB = fma2(uB, two, pack2(-p.z, -p.w));
+  // c*lap packed; its unpacked halves feed scalar adds, which ptxas does not
+  // contract (checked in the SASS: no scalar FFMA in this kernel)
   const f32x2 cc = pack2(c, c);
   const f32x2 clA = mul2(cc, lapA), clB = mul2(cc, lapB);
-  float l0, l1, l2, l3, f0, f1, f2, f3;
+  float l0, l1, l2, l3, t0, t1, t2, t3;
   unpack2(clA, l0, l1);
   unpack2(clB, l2, l3);
-  unpack2(fA, f0, f1);
-  unpack2(fB, f2, f3);
+  unpack2(tA, t0, t1);
+  unpack2(tB, t2, t3);
   float4 o;
-  o.x = __fsub_rn(l0, f0);
-  o.y = __fsub_rn(l1, f1);
-  o.z = __fsub_rn(l2, f2);
-  o.w = __fsub_rn(l3, f3);
+  o.x = __fadd_rn(t0, l0);
+  o.y = __fadd_rn(t1, l1);
+  o.z = __fadd_rn(t2, l2);
+  o.w = __fadd_rn(t3, l3);
   return o;
 }
 template <typename Vec>

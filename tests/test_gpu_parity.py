@@ -199,7 +199,9 @@ def test_fused_wave_chain_fast_form_bit_exact(scale, c):
     block's magnitude bound allows it (cq_wave5_fused_bounded); large, tiny
     and ordinary fields over many blocks stay bit-identical to the oracle."""
     from paper_2505_06022_b200.executor import Placement, Session
-    h, w, steps = 515, 640, 64
+    # wide enough for interior CTAs (only those take the FMA form: a 12-warp
+    # KL=8 block spans 12 x 112 columns plus halos)
+    h, w, steps = 768, 3072, 64
     rng = np.random.default_rng(31)
     u0 = (rng.uniform(-1, 1, (h, w)) * scale).astype(np.float32)
     up0 = (rng.uniform(-1, 1, (h, w)) * scale).astype(np.float32)
@@ -213,6 +215,30 @@ def test_fused_wave_chain_fast_form_bit_exact(scale, c):
         s.close()
         u, up = onat.wave_run(u0, up0, steps, c)
         assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up), (scale, c, nodes)
+
+
+@pytest.mark.parametrize("c", [0.3, -0.2])
+def test_fused_wave_chain_fast_form_signed_zeros(c):
+    """Fields of +0 / -0 and the smallest subnormals: exact cancellations
+    (2u == p) and products underflowing to -0 must give the tree's signed
+    zeros in the FMA form too (t = fma(2, u, -p), not -fma(-2, u, p))."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    h, w, steps = 768, 3072, 40   # interior CTAs exist (see above)
+    rng = np.random.default_rng(33)
+    vals = np.array([0.0, -0.0, 1e-45, -1e-45, 3e-45, -3e-45], dtype=np.float32)
+    u0 = vals[rng.integers(0, len(vals), (h, w))]
+    up0 = vals[rng.integers(0, len(vals), (h, w))]
+    up0[::3] = u0[::3] * np.float32(2)   # exact cancellations 2u - p == 0
+    for nodes in (1, 3):
+        prog = W.wave_program(h, w, steps=steps, kind="float32", c=c, u0=u0, up0=up0)
+        s_ = Session(cq.generate_commands(prog.graph(), nodes), Placement(1, 0, (0,)))
+        assert s_.chains and len(s_.chains[0].blocks) >= 4
+        s_.execute(upload=True)
+        s_.synchronize()
+        res = s_.results()
+        s_.close()
+        u, up = onat.wave_run(u0, up0, steps, c)
+        assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up), (c, nodes)
 
 
 def test_fused_wave_graph_replay_continues_the_simulation():
