@@ -151,12 +151,13 @@ def test_fused_wave_chain_bit_exact_vs_oracle(nodes, steps, c):
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
 
 
-@pytest.mark.parametrize("nodes,steps", [(1, 22), (3, 16)])
-def test_fused_wave_chain_float64_bit_exact(nodes, steps):
+@pytest.mark.parametrize("nodes,steps,w", [(1, 22, 384), (3, 16, 384), (1, 22, 1280), (3, 16, 1280)])
+def test_fused_wave_chain_float64_bit_exact(nodes, steps, w):
     """The float64 fused kernel (two doubles per lane, scalar DADD/DMUL) is
-    bit-identical to the float64 per-step oracle."""
+    bit-identical to the float64 per-step oracle (w = 1280 has interior
+    CTAs: 8 warps x 48 columns per block)."""
     from paper_2505_06022_b200.executor import Placement, Session
-    h, w = 517, 384
+    h = 517
     u0 = np.random.default_rng(41).uniform(0, 1, (h, w))
     up0 = np.random.default_rng(42).uniform(0, 1, (h, w))
     u0[:, :5] *= 1e-300
