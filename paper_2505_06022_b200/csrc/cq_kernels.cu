@@ -714,10 +714,10 @@ struct FusedShape {
   // kOldInSmem keeps the rows two iterations old of every level in shared
   // memory (each is read once more, as the north neighbour one level up and
   // as u_prev two levels up), freeing ~32 registers: for KL = 8, V = 4 that
-  // fits two 6-warp blocks per SM without spills, but measured slower
-  // (16.7 vs 20.8 TB/s: the extra LDS/STS per level cost more than the 12
-  // warps gain), so the register-only variant runs one 8-warp block per SM
-  // (~200 registers).
+  // fitted two 6-warp blocks per SM without spills when the kernel needed
+  // ~200 registers, but measured slower (16.7 vs 20.8 TB/s: the extra
+  // LDS/STS per level cost more than the 12 warps gained); the register-only
+  // kernel now reaches 12 warps per SM by itself (see above).
   static constexpr bool kOldInSmem = false;
   static constexpr int kWarps = (KL == 8 && V == 4) ? 12 : 8;
   static constexpr int kMinBlocks = KL == 8 ? 1 : 2;
@@ -1060,8 +1060,8 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
              (long long)out_lo, (long long)out_hi, (long long)in_lo, (long long)in_hi);
   // tuning: CQ_WAVE_FUSED_CFG="V,D,RB" (lane width, cp.async ring depth,
   // upper bound on rows per block, see fused_segment); default 4,6,128 for
-  // KL = 4 (2 blocks / SM) and 4,6,256 for KL = 8 (1 block / SM: its 8
-  // register windows need ~200 regs)
+  // KL = 4 (two 8-warp blocks / SM) and 4,6,256 for KL = 8 (one 12-warp
+  // block / SM: its 8 levels of register windows need ~153 registers)
   static int cfg_env = [] {
     int v = 0, d = 0, rb = 0;
     if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d,%d", &v, &d, &rb);
