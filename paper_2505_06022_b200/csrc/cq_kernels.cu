@@ -707,8 +707,9 @@ __device__ __forceinline__ void cp_async_wait() {
 // with 32-bit row counters and running prefetch pointers it needs ~153
 // registers, under the 168 that 3 warps per SM sub-partition allow (the
 // earlier 64-bit row arithmetic needed ~200 and capped it at 8 warps;
-// 12 warps then spilled, profiles/r01/fused_cfg_sweep.log).  Other shapes
-// run 8-warp blocks.
+// 12 warps then spilled, profiles/r01/fused_cfg_sweep.log).  16 warps
+// (128 registers) spill 72 bytes a thread and measured 11% slower
+// (profiles/r01/w16_ab.log).  Other shapes run 8-warp blocks.
 template <int KL, int V>
 struct FusedShape {
   // kOldInSmem keeps the rows two iterations old of every level in shared
