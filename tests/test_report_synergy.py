@@ -109,3 +109,25 @@ def test_bench_clock_sweep_leg_on_the_simulated_device(monkeypatch):
         assert len(out[name]["points"]) == 3
         assert set(out[name]["selected_mhz"]) == {"MAX_PERF", "MIN_ENERGY", "MIN_EDP", "MIN_ED2P"}
         assert out[name]["selected_mhz"]["MAX_PERF"] == 1965
+
+
+def test_bench_reference_arm_contract_line():
+    """`bench.py --impl reference` (the CPU port of the path, no GPU) prints
+    one JSON line with the contract's keys; W is raised to the minimum 3."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--size", "256",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["warmup"] >= 3 and d["steps"] == 2
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("port", "reference")
+    assert d["value"] > 0 and d["cpu_baseline"]["value"] == d["value"]
