@@ -321,6 +321,39 @@ def test_sgemm_within_tolerance(variant, nodes):
     assert err.max() <= 1e-6, err.max()
 
 
+def test_fused_pass_rejects_bad_arguments():
+    """The C-ABI fails loudly (NativeError with the reason) on arguments the
+    fused pass cannot honour, instead of computing something else."""
+    import ctypes
+    import torch
+    from paper_2505_06022_b200 import _native as N
+    N.call("cq_init_device", 0)
+    h, w = 64, 256
+    t = [torch.zeros((h, w), device="cuda") for _ in range(4)]
+
+    def view(x):
+        v = N.CqView()
+        v.ptr = x.data_ptr()
+        v.alloc = N.box3((0, 0), (h, w))
+        v.stride[:] = [h * w, w, 1]
+        return v
+    vs = [view(x) for x in t]
+    ext = N.box3((0, 0), (h, w))
+
+    def call(levels=8, out=(0, h), views=vs, k2=2.0):
+        N.call("cq_wave5_fused_bounded", 0, 0, N.CQ_F32, levels, ctypes.byref(views[0]), ctypes.byref(views[1]),
+               ctypes.byref(views[2]), ctypes.byref(views[3]), 0, h, out[0], out[1], ctypes.byref(ext), 0.25,
+               k2, 4.0, None, None)
+    call()   # valid
+    N.call("cq_stream_synchronize", 0, 0)
+    with pytest.raises(cq.NativeError, match="levels"):
+        call(levels=5)
+    with pytest.raises(cq.NativeError, match="alias"):
+        call(views=[vs[0], vs[1], vs[0], vs[3]])
+    with pytest.raises(cq.NativeError, match="constants"):
+        call(k2=3.0)
+
+
 def test_integer_division_by_zero_raises_eval_error():
     ext = cq.Box.from_shape((16,))
     bufs = {"a": cq.Buffer("a", ext, "int64", cq.BufferInit.iota()),
