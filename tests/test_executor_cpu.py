@@ -148,7 +148,7 @@ def _rank_main(rank, world, port, outdir):
     for nodes in (2, 3):
         prog = W.wave_program(160, 32, steps=14, kind="float32", u0=fu0, up0=fu0)
         sess = E.Session(cq.generate_commands(prog.graph(), nodes), pl)
-        assert [b.kl for b in sess.chains[0].blocks] == [8, 4]
+        assert [b.kl for b in sess.chains[0].blocks] == [4, 8]
         sess.execute(upload=True)
         sess.synchronize()
         res = sess.results()
@@ -316,7 +316,7 @@ def test_fused_chain_disabled_and_graph_replay(fake, monkeypatch):
     s0.close()
     monkeypatch.delenv("CQ_WAVE_FUSE")
     s = E.Session(plan, E.Placement(1, 0, (0,)))
-    assert [b.kl for b in s.chains[0].blocks] == [8, 4]
+    assert [b.kl for b in s.chains[0].blocks] == [4, 8]
     s.execute(upload=True)
     s.synchronize()
     s.recycle()
@@ -368,7 +368,7 @@ def test_fused_wave_chain_float64(fake):
     prog = W.wave_program(h, w, steps=steps, kind="float64", c=0.3, u0=u0, up0=u0)
     s = E.Session(cq.generate_commands(prog.graph(), 2), E.Placement(1, 0, (0,)))
     ch = s.chains[0]
-    assert [b.kl for b in ch.blocks] == [8, 4, 4, 4] and len(ch.plain) == 2
+    assert [b.kl for b in ch.blocks] == [4, 8, 4, 4] and len(ch.plain) == 2
     s.execute(upload=True)
     s.synchronize()
     res = s.results()
