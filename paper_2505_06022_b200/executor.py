@@ -434,6 +434,9 @@ class Session:
         self.launch_log = []    # (binding kind, cells, device, start, stop) per kernel launch
         self.capturing = False
         self.graph = None
+        self.graphs = []        # one graph, or two alternating ones (odd fused chains)
+        self._graph_logs = []
+        self._phase = 0         # which of two graphs launches next
         self.graph_log = []     # launch_log of a timed capture: its events re-record per replay
         self.graph_events = []
         self.host_init = {}
@@ -1169,12 +1172,29 @@ class Session:
             elif self.local(step[1].node):
                 self.exec_command(step[1], step[2])
 
+    def _odd_chains(self):
+        """Fused chains with an odd number of out-of-place blocks: one run
+        leaves their current fields in the alternate allocations."""
+        return [ch for ch in self.chains if len(ch.blocks) % 2]
+
+    def _toggle_odd_chains(self):
+        """Swap current and alternate allocations of the odd chains (what one
+        run of them does on the device)."""
+        for ch in self._odd_chains():
+            for node in ch.rows:
+                if self.local(node):
+                    for buf in (ch.a, ch.b):
+                        self.views[(node, buf)], self.alt[(node, buf)] = \
+                            self.alt[(node, buf)], self.views[(node, buf)]
+
     def capture(self, timed: bool = False):
         """Capture one replay of the plan (``execute(upload=False)``) into a
         CUDA graph -- kernels, copies, NCCL groups and the cross-stream event
         edges -- so later replays cost one launch instead of one Python
         dispatch per command.  One local device only (the one-rank-per-GPU
-        layout).
+        layout).  When a fused chain has an odd number of blocks, a run ends
+        on the other allocations, so two graphs are captured (from either
+        allocation) and ``replay`` alternates them.
 
         timed=True brackets every launch with event-record nodes; after each
         replay (and a synchronize) ``graph_log`` holds that replay's per-launch
@@ -1184,46 +1204,70 @@ class Session:
         d = self.devices[0]
         self.synchronize()
         self.recycle()
+        self._drop_graph()
         saved = self.want_trace
-        self.want_trace = timed
-        self.capturing = True
-        N.call("cq_graph_begin", d)
-        handle = ctypes.c_uint64()
+        graphs, logs, events, scratch = [], [], [], []
         try:
-            self.execute(upload=False)
-        except Exception:
-            try:
+            for _k in range(2 if self._odd_chains() else 1):
+                self.want_trace = timed
+                self.capturing = True
+                N.call("cq_graph_begin", d)
+                handle = ctypes.c_uint64()
+                try:
+                    self.execute(upload=False)
+                except Exception:
+                    try:
+                        N.call("cq_graph_end", d, ctypes.byref(handle))
+                        N.call("cq_graph_destroy", handle)
+                    except NativeError:
+                        pass
+                    raise
+                finally:
+                    self.capturing = False
+                    self.want_trace = saved
                 N.call("cq_graph_end", d, ctypes.byref(handle))
-                N.call("cq_graph_destroy", handle)
-            except NativeError:
-                pass
-            self.want_trace, self.capturing = saved, False
+                graphs.append(handle.value)
+                # pack/unpack temporaries allocated while capturing belong to the graph
+                scratch += self.scratch
+                self.scratch = []
+                logs.append(list(self.launch_log) if timed else [])
+                if timed:
+                    # the graph's event-record nodes own these events: keep them
+                    # out of the recycling pool for the graph's lifetime
+                    events += [ev for _d, _t, ev in self.events]
+                    self.events = []
+                self.recycle()  # other events recorded during capture are graph-internal
+        except Exception:
+            for g in graphs:
+                N.call("cq_graph_destroy", ctypes.c_uint64(g))
+            _free_scratch(scratch)
+            for ev in events:
+                N.call("cq_event_destroy", ctypes.c_uint64(ev))
+            if len(graphs) % 2:   # one capture's view swaps without its partner
+                self._toggle_odd_chains()
             self.recycle()
             raise
-        finally:
-            self.capturing = False
-        N.call("cq_graph_end", d, ctypes.byref(handle))
-        self.want_trace = saved
-        self._drop_graph()
-        # pack/unpack temporaries allocated while capturing belong to the graph
-        self._graph_scratch, self.scratch = self.scratch, []
-        log = list(self.launch_log)
-        if timed:
-            # the graph's event-record nodes own these events: keep them out
-            # of the recycling pool for the graph's lifetime
-            self.graph_events = [ev for _d, _t, ev in self.events]
-            self.events = []
-        self.recycle()  # other events recorded during capture are graph-internal
-        self.graph = handle.value
-        self.graph_log = log if timed else []
+        # capturing executed nothing: with two graphs the views are back where
+        # the device state is (the second capture started where the first ended)
+        self._graph_scratch = scratch
+        self.graph_events = events
+        self.graphs = graphs
+        self._graph_logs = logs
+        self._phase = 0
+        self.graph = graphs[0]
+        self.graph_log = logs[0]
         return self.graph
 
     def _drop_graph(self):
         if self.graph:
             for d in self.devices:
                 N.call("cq_stream_synchronize", d, N.STREAM_COMPUTE)
-            N.call("cq_graph_destroy", ctypes.c_uint64(self.graph))
+            for g in self.graphs or [self.graph]:
+                N.call("cq_graph_destroy", ctypes.c_uint64(g))
             self.graph = None
+        self.graphs = []
+        self._graph_logs = []
+        self._phase = 0
         for ev in self.graph_events:
             N.call("cq_event_destroy", ctypes.c_uint64(ev))
         self.graph_events = []
@@ -1231,9 +1275,15 @@ class Session:
         _free_scratch(self._graph_scratch)
 
     def replay(self, times: int = 1):
-        """Launch the captured graph ``times`` times (asynchronous)."""
+        """Launch the captured graph ``times`` times (asynchronous); with two
+        graphs (odd chains) they alternate and the views follow."""
         for _ in range(times):
-            N.call("cq_graph_launch", ctypes.c_uint64(self.graph), self.devices[0])
+            N.call("cq_graph_launch", ctypes.c_uint64(self.graphs[self._phase] if self.graphs else self.graph),
+                   self.devices[0])
+            if len(self.graphs) == 2:
+                self.graph_log = self._graph_logs[self._phase]
+                self._phase ^= 1
+                self._toggle_odd_chains()
 
     def mark(self):
         """Join all streams of every local device and record a timing event

@@ -172,21 +172,16 @@ def _halo_pushes_ok(pushes, ubuf, rows, W):
 
 
 def _blocks(tids, kind="float32"):
-    """Split a chain into out-of-place blocks with an even count (so the
-    current allocations return to where they started): as many KL=8 blocks
-    as the parity allows (KL=8 moves half the bytes per step of KL=4) plus
-    KL=4 blocks, one of them first.  Tasks left over (< 4) run plain."""
+    """Split a chain into out-of-place blocks: as many KL=8 blocks as fit
+    (KL=8 moves half the bytes per step of KL=4) and a KL=4 block for a
+    remaining quarter, placed first -- a run's first block has no magnitude
+    bound and keeps the exact form, which costs the HBM-bound 4-step pass
+    nothing but the FP-bound 8-step pass ~15% (cq_wave5_fused_bounded).  An
+    odd block count leaves a run's fields in the alternate allocations; the
+    executor follows them, and graph capture then records two alternating
+    graphs.  Tasks left over (< 4) run plain."""
     q, _r = divmod(len(tids), KL_BASE)   # quarter blocks
-    b = q % 2                          # KL=4 blocks (same parity as q)
-    a = (q - b) // 2                   # KL=8 blocks
-    if (a + b) % 2:
-        a, b = a - 1, b + 2
-    if a < 0:
-        return [], tuple(tids)
-    # a KL=4 block goes first: the first block of a run has no magnitude
-    # bound and keeps the exact form, which costs the HBM-bound 4-step pass
-    # nothing but the FP-bound 8-step pass ~15% (cq_wave5_fused_bounded)
-    sizes = ([KL_BASE] if b else []) + [KL_PARITY] * a + [KL_BASE] * max(b - 1, 0)
+    sizes = [KL_BASE] * (q % 2) + [KL_PARITY] * (q // 2)
     if not sizes:
         return [], tuple(tids)
     blocks, i = [], 0

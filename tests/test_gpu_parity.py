@@ -497,7 +497,7 @@ def test_wave_baseline_size_bit_exact():
     for nodes in (1, 4):
         prog = W.wave_program(n, n, steps=steps, kind="float32", c=0.25, u0=u0, up0=u0)
         s = Session(cq.generate_commands(prog.graph(), nodes), Placement(1, 0, (0,)), trace=False)
-        assert [b.kl for b in s.chains[0].blocks] == [4] + [8] * 11 + [4] * 2
+        assert [b.kl for b in s.chains[0].blocks] == [4] + [8] * 12
         s.execute(upload=True)
         s.synchronize()
         res = s.results()
