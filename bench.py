@@ -365,7 +365,7 @@ def bench_wave(args, dist, placement, peaks):
                               "and writing two levels (16 B/cell, ncu traffic above), so the algorithmic "
                               "12 B/cell/step rate exceeds the HBM peak; the pass itself is FP32-pipe / issue "
                               "limited (ncu, FMA form, 12 warps/SM: FMA pipe 67% active, issue 70% busy, "
-                              "profiles/r01/wave5_fused8_ncu_full_summary.txt)")
+                              "profiles/r01/wave5_fused8_ncu_full_summary_r67.txt)")
                              if dom_kind == "wave5_fused8" else None,
                      "launch_timing": timing_source},
         "clocks": clk,
