@@ -48,6 +48,34 @@ SWEEP_SECONDS = 1.0   # NVML energy window per clock point
 C = 0.25
 
 
+def _baseline_metric():
+    """BASELINE.json's metric string, printed verbatim by BOTH arms (the
+    driver pairs the b200 and reference lines by metric, unit and
+    higher_is_better)."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as fh:
+            return json.load(fh)["metric"]
+    except (OSError, KeyError, ValueError):
+        return "GB/s (or GFLOP/s) per kernel at 1/2/4/8 B200, % roofline; J/iteration vs SM clock"
+
+
+METRIC = _baseline_metric()
+UNIT = "GB/s"
+# what `value` measures under that metric (both arms)
+METRIC_DETAIL = ("wave_sim 5-point stencil, 12 B x cells x time steps / time (SURVEY.md §8d: read u, "
+                 "read u_prev, write u_next per cell per time step)")
+
+
+def headline_config(size, world, wave_steps):
+    """The headline workload (BASELINE configs[1]), identical in both arms."""
+    return {"workload": f"wave_sim 2-D 5-point stencil {size}x{size} fp32 per GPU (global {size * world}x{size}), "
+                        f"{wave_steps} time steps per bench step, neighborhood(1,1) halo exchange",
+            "metric_detail": METRIC_DETAIL,
+            "parallelism": f"dp{world} (row slabs, one rank per GPU)",
+            "l2": "inputs 2 GiB/GPU >> 126 MB L2 (no flush needed)",
+            "init": "Gaussian pulse (SURVEY.md §8d)"}
+
+
 def _env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -192,6 +220,28 @@ def wave_inputs(h, w, rows):
     return u0, up0
 
 
+def pulse_field(h, w):
+    """The same Gaussian pulse as ``wave_inputs`` as a plain host array (the
+    CPU arms)."""
+    out = np.empty((h, w), np.float32)
+    j = np.arange(w, dtype=np.float64)[None, :] - w / 2
+    jj = j * j
+    s2 = 2 * (w / 16.0) ** 2
+    for r0 in range(0, h, 1024):
+        r1 = min(r0 + 1024, h)
+        i = np.arange(r0, r1, dtype=np.float64)[:, None] - h / 2
+        out[r0:r1] = np.exp(-(i * i + jj) / s2).astype(np.float32)
+    return out
+
+
+def sm_count():
+    try:
+        import torch
+        return torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:  # noqa: BLE001
+        return 148
+
+
 def bench_wave(args, dist, placement, peaks):
     import paper_2505_06022_b200 as cq
     from paper_2505_06022_b200 import executor as E
@@ -294,14 +344,9 @@ def bench_wave(args, dist, placement, peaks):
     dev_ms = dist.max(dev_ms)
     cells = H * Wd * steps * args.steps
     value = 12 * cells / (dev_ms / 1e3) / 1e9
-    # roofline numerator per the contract: SURVEY §8d's algorithmic figure
-    # (12 B per cell per time step) x the units one launch processes (its
-    # cells x the time steps it advances); the kernel's own minimum traffic
-    # (16 B/cell per fused pass) is reported beside it
     steps_per_launch = {"wave5_fused8": 8, "wave5_fused4": 4}.get(dom_kind, 1)
     kern_s = kern_ms / 1e3
-    achieved = dist.min(12 * steps_per_launch * (kern_bytes / bpc) / kern_s / 1e9)
-    achieved_own = dist.min(kern_bytes / kern_s / 1e9)
+    cells_launch = kern_bytes / bpc   # output cells of the timed launches
     clk = clocks.summary()
 
     # ---- end to end through the public API, host buffers ------------------
@@ -335,13 +380,8 @@ def bench_wave(args, dist, placement, peaks):
     field = res_buffers[newest][lo:hi]
     finite = bool(np.isfinite(field).all())
 
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"{dom_kind}_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            t = json.load(fh)
-        if t.get("cells"):
-            traffic = t["dram_bytes"] / t["cells"] * dom_launch[1]
+    roofline = wave_roofline(dom_kind, dom_launch[1], len(dominant), cells_launch, kern_s, steps_per_launch,
+                             bpc, clk, peaks, dist, placement.devices[0], Wd, timing_source)
 
     return {
         "value": value, "ms_per_step": dev_ms / args.steps, "plan_s": plan_s,
@@ -350,24 +390,7 @@ def bench_wave(args, dist, placement, peaks):
                 "api": f"executor.run_batch (depth {depth}: upload, kernels and read-back of simulations overlap)",
                 "sync": {"value": 12 * cells / sync_s / 1e9, "ms_per_step": sync_s * 1e3 / args.steps,
                          "api": "executor.run (one simulation at a time)"}},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0]["hbm_gbs"],
-                     "unit": "GB/s", "frac": achieved / peaks[0]["hbm_gbs"], "traffic": traffic,
-                     "kernel": {"wave5_fused8": "wave5_fused_kernel<float,8,4,6,256> (8 time steps per pass)",
-                                "wave5_fused4": "wave5_fused_kernel<float,4,4,6,128> (4 time steps per pass)"}.get(
-                                    dom_kind, "wave5_rows_kernel<float,32>"),
-                     "algorithmic_bytes_per_cell_step": 12, "time_steps_per_launch": steps_per_launch,
-                     "cells_per_launch": dom_launch[1], "launches": len(dominant),
-                     "bytes_per_launch": 12 * steps_per_launch * dom_launch[1],
-                     "kernel_bytes_per_cell": bpc, "achieved_kernel_traffic": achieved_own,
-                     "frac_kernel_traffic": achieved_own / peaks[0]["hbm_gbs"],
-                     "peak_source": peaks[1] + " hbm_gbs (torch copy)",
-                     "note": ("temporal blocking: one launch advances 8 time steps while reading X(t), X(t-1) "
-                              "and writing two levels (16 B/cell, ncu traffic above), so the algorithmic "
-                              "12 B/cell/step rate exceeds the HBM peak; the pass itself is FP32-pipe / issue "
-                              "limited (ncu, FMA form, 12 warps/SM: FMA pipe 67% active, issue 70% busy, "
-                              "profiles/r01/wave5_fused8_ncu_full_summary_r67.txt)")
-                             if dom_kind == "wave5_fused8" else None,
-                     "launch_timing": timing_source},
+        "roofline": roofline,
         "clocks": clk,
         "gpu_launches": gpu_launches,
         "replay": replay_mode,
@@ -375,6 +398,73 @@ def bench_wave(args, dist, placement, peaks):
         "execution": execution,
         "H": H, "W": Wd,
     }
+
+
+def wave_roofline(kind, cells_per_launch, launches, cells_timed, kern_s, levels, bpc, clk, peaks, dist, device,
+                  width, timing_source):
+    """Roofline of the dominant wave kernel against the resource that binds it.
+
+    * one-step kernel / KL=4 pass: HBM.  achieved = the kernel's own minimum
+      traffic (12 B/cell one-step, 16 B/cell per fused pass: read X(t),
+      X(t-1), write two levels) over its CUDA-event launch time.
+    * KL=8 pass: FP32 pipe / issue (ncu: FMA pipe and issue ~70% busy, DRAM
+      below peak).  achieved = USEFUL FP32 lane-ops -- 7 per cell per level
+      (n+s, +w, +e, fma(-4,u,.), fma(2,u,-p), c*lap, +), recompute
+      of halo columns / rows not counted -- over the launch time; peak =
+      SMs x 128 lanes x the SM clock observed in the timed region.  The DRAM
+      fraction (ncu bytes), the recompute share (launch geometry) and the
+      12-B/cell/step rate (``effective_gbs``) are reported beside it."""
+    from paper_2505_06022_b200 import _native as N
+    import ctypes
+    hbm = peaks[0]["hbm_gbs"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"{kind}_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            t = json.load(fh)
+        if t.get("cells"):
+            traffic = t["dram_bytes"] / t["cells"] * cells_per_launch
+    effective = dist.min(12 * levels * cells_timed / kern_s / 1e9)
+    own = dist.min(bpc * cells_timed / kern_s / 1e9)
+    names = {"wave5_fused8": "wave5_fused_kernel<float,8,4,6,256> (8 time steps per pass)",
+             "wave5_fused4": "wave5_fused_kernel<float,4,4,6,128> (4 time steps per pass)"}
+    out = {"kernel": names.get(kind, "wave5_rows_kernel<float,32>"), "cells_per_launch": cells_per_launch,
+           "launches": launches, "time_steps_per_launch": levels, "launch_timing": timing_source,
+           "effective_gbs": effective, "effective_note": "12 B x cells x time steps per launch / launch time "
+                                                          "(SURVEY §8d unit; not a traffic rate)",
+           "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                           f"(profiles/{kind}_traffic.json)"}
+    if kind != "wave5_fused8":
+        out.update({"bound": "hbm", "achieved": own, "peak": hbm, "unit": "GB/s", "frac": own / hbm,
+                    "traffic": traffic, "algorithmic_bytes_per_cell": bpc,
+                    "peak_source": peaks[1] + " hbm_gbs (torch copy)"})
+        return out
+    sms = sm_count()
+    mhz = clk.get("sm_mhz") or peaks[0].get("sm_max_mhz", 1965.0)
+    mx = peaks[0].get("sm_max_mhz", 1965.0)
+    ops = 7 * levels * cells_timed / kern_s / 1e9        # useful G lane-ops/s
+    ops = dist.min(ops)
+    peak = sms * 128 * mhz / 1e3                          # G lane-ops/s at the observed clock
+    geo = (ctypes.c_int64 * 4)()
+    try:
+        N.call("cq_wave5_fused_geometry", device, N.CQ_F32, levels, cells_per_launch // width, width, geo)
+        computed = geo[3]
+        recompute = 1.0 - cells_per_launch / computed
+        geometry = {"rows_per_block": geo[0], "grid": [geo[1], geo[2]], "computed_cells_per_level": computed}
+    except Exception as exc:  # noqa: BLE001
+        recompute, geometry = None, {"error": str(exc)[:200]}
+    launch_s = kern_s * cells_per_launch / cells_timed   # average launch duration
+    dram_gbs = traffic / launch_s / 1e9 if traffic else None
+    out.update({"bound": "fp32_issue", "achieved": ops, "peak": peak, "unit": "G FP32 lane-ops/s",
+                "frac": ops / peak, "traffic": traffic,
+                "peak_definition": f"{sms} SMs x 128 FP32 lanes x {mhz:.0f} MHz (median SM clock in the timed "
+                                   "region), one lane-op per lane per cycle",
+                "peak_at_max_clock": sms * 128 * mx / 1e3, "frac_at_max_clock": ops / (sms * 128 * mx / 1e3),
+                "useful_ops_per_cell_level": 7, "recompute_share": recompute, "geometry": geometry,
+                "dram": {"achieved_gbs": dram_gbs, "peak_gbs": hbm,
+                         "frac": dram_gbs / hbm if dram_gbs else None,
+                         "kernel_min_bytes_per_cell": bpc, "achieved_min_bytes_gbs": own}})
+    return out
 
 
 # -------------------------------------------------------- other BASELINE kernels
@@ -661,39 +751,92 @@ def cpu_wave_baseline(seconds=12.0, size=SIZE):
                                       f"(oracle/cq_oracle.c, OpenMP, {os.cpu_count()} threads)"}
 
 
+def cpu_kernel_baselines(args, seconds=4.0):
+    """SURVEY §8d's CPU-side column for SAXPY, N-body and matmul: the C port
+    (oracle/cq_oracle.c, OpenMP over every host thread) on bounded samples
+    of the same workloads, ~``seconds`` each."""
+    _all_host_threads()
+    from oracle import native as onat
+    from paper_2505_06022_b200 import workloads as W
+    cores = os.cpu_count()
+    out = {}
+
+    def loop(fn):
+        fn()  # warm
+        t0 = time.perf_counter()
+        n = 0
+        while time.perf_counter() - t0 < seconds:
+            fn()
+            n += 1
+        return n, time.perf_counter() - t0
+
+    n = 1 << 24
+    x, y = W.saxpy_inputs(n, "float32", seed=0)
+    reps, dt = loop(lambda: onat.saxpy(2.0, x, y))
+    out["saxpy_2p24_4chunks"] = {"value": 12 * n * reps / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+                                 "sample": f"{reps} fp32 SAXPY passes over 2^24 elements (12 B/element)"}
+    nb = args.nbody
+    pos, _vel = W.nbody_inputs(nb)
+    ni = 64
+    reps, dt = loop(lambda: onat.nbody_accel(pos, 0, ni, 1e-2))
+    out["nbody_262144"] = {"value": 20 * ni * nb * reps / dt / 1e9, "unit": "GFLOP/s", "cores": cores,
+                           "kind": "port",
+                           "sample": f"{reps} x {ni} i-bodies x all {nb} j (float64 accumulation, fixed j order; "
+                                     "20 flop/interaction)"}
+    m = args.sgemm
+    rng = np.random.default_rng(5)
+    a = rng.uniform(-1, 1, (8, m)).astype(np.float32)
+    b = rng.uniform(-1, 1, (m, m)).astype(np.float32)
+    rows = np.arange(8)
+    reps, dt = loop(lambda: onat.sgemm_rows(a, b, rows, with_abs=False))
+    out["sgemm"] = {"value": 2 * 8 * m * m * reps / dt / 1e9, "unit": "GFLOP/s (useful 2MNK)", "cores": cores,
+                    "kind": "port", "sample": f"{reps} x 8 rows of C = A B at K = N = {m} (float64 accumulation, "
+                                              "fixed k order)"}
+    return out
+
+
 def reference_arm(args, dist):
     """--impl reference: the reference's CPU implementation of the path on the
-    host cores.  The reference is pure Python (clusterq) and does not travel
-    to the GPU box, so this times its C restatement (oracle/), all threads."""
+    host cores.  The reference is pure Python (clusterq, ~50 us per cell) and
+    does not travel to the GPU box, so this times its C restatement
+    (oracle/cq_oracle.c, OpenMP over every host thread) on the b200 arm's
+    workload: each bench step is one full ``--wave-steps`` simulation of one
+    GPU's 16384 x 16384 fp32 slab from the same Gaussian pulse.  At N > 1 the
+    whole job is N such slabs; the CPU's rate does not depend on how many, so
+    one slab per step is the bounded sample (rank 0 alone runs)."""
     if dist.rank != 0:
         return None
     _all_host_threads()
     from oracle import native as onat
-    size = args.size
-    u = np.random.default_rng(2).uniform(0, 1, (size, size)).astype(np.float32)
-    up = u.copy()
+    size, nsteps = args.size, args.wave_steps
+    u0 = pulse_field(size, size)
+
+    def simulate():
+        # ping-pong as workloads.wave_program: even steps write up, odd steps u
+        u, up = u0.copy(), u0.copy()
+        for s in range(nsteps):
+            if s % 2 == 0:
+                onat.wave_step(u, up, C, out=up)
+            else:
+                onat.wave_step(up, u, C, out=u)
+
     for _ in range(args.warmup):
-        onat.wave_step(u, up, C, out=up)
+        simulate()
     t0 = time.perf_counter()
-    for s in range(args.steps):
-        if s % 2 == 0:
-            onat.wave_step(u, up, C, out=up)
-        else:
-            onat.wave_step(up, u, C, out=u)
+    for _ in range(args.steps):
+        simulate()
     dt = time.perf_counter() - t0
-    val = 12 * size * size * args.steps / dt / 1e9
+    val = 12 * size * size * nsteps * args.steps / dt / 1e9
+    sample = (f"{args.steps} x {nsteps}-step simulations of one {size}x{size} fp32 slab (Gaussian pulse), "
+              f"oracle/cq_oracle.c OpenMP {os.cpu_count()} threads"
+              + (f"; the {args.gpus}-GPU job is {args.gpus} such slabs" if args.gpus > 1 else ""))
     return {
-        "metric": "wave_sim 5-pt stencil effective HBM bandwidth (GB/s, 12 B/cell/step)",
-        "impl": "reference", "value": val, "unit": "GB/s", "n_gpus": args.gpus,
+        "metric": METRIC, "impl": "reference", "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": f"wave_sim 2-D 5-point stencil {size}x{size} fp32 per GPU, 1 time step "
-                               f"per bench step (bounded CPU sample of the 100-step run)"},
-        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": f"{args.steps} wave steps of {size}x{size} fp32, "
-                                   f"oracle/cq_oracle.c OpenMP {os.cpu_count()} threads"},
-        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic", "config": headline_config(size, args.gpus, nsteps),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
@@ -732,6 +875,24 @@ def clock_sweep(args, dist, placement):
         out[name] = entry
         sess.close()
     return out
+
+
+def headline_line(args, world, wave, cpu, kernels, sweep):
+    """The b200 arm's JSON line; metric, unit, higher_is_better and config
+    are the reference arm's (``reference_arm``) byte for byte."""
+    return {
+        "metric": METRIC, "impl": "b200", "value": wave["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wave["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": headline_config(args.size, world, args.wave_steps),
+        "run": {"plan_s": wave["plan_s"], "replay": wave["replay"], "execution": wave["execution"],
+                "kernels_note": "per-kernel GB/s | GFLOP/s and % roofline of the other BASELINE workloads "
+                                "are under 'kernels'"},
+        "e2e": wave["e2e"], "roofline": wave["roofline"], "cpu_baseline": cpu,
+        "clocks": wave["clocks"], "gpu_launches": wave["gpu_launches"],
+        "energy": {"wave5": wave["energy"], "clock_sweep": sweep},
+        "kernels": kernels,
+    }
 
 
 def main():
@@ -776,26 +937,15 @@ def main():
     cpu = None
     if dist.world == 1 and dist.rank == 0 and not args.no_cpu:
         cpu = cpu_wave_baseline()
+        if kernels is not None:
+            base = cpu_kernel_baselines(args)
+            for key, entry in kernels.items():
+                for name, b in base.items():
+                    if key.startswith(name) and isinstance(entry, dict):
+                        entry["cpu_baseline"] = b
     if dist.rank == 0:
-        line = {
-            "metric": "wave_sim 5-pt stencil effective HBM bandwidth (GB/s, 12 B/cell/step), "
-                      "plus per-kernel GB/s|GFLOP/s and % roofline",
-            "value": wave["value"], "unit": "GB/s", "n_gpus": dist.world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": wave["ms_per_step"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"wave_sim 2-D 5-point stencil {args.size}x{args.size} fp32 per GPU "
-                                   f"(global {wave['H']}x{wave['W']}), {args.wave_steps} time steps per "
-                                   f"bench step, neighborhood(1,1) halo exchange",
-                       "parallelism": f"dp{dist.world} (row slabs, one rank per GPU)",
-                       "l2": "inputs 2 GiB/GPU >> 126 MB L2 (no flush needed)",
-                       "plan_s": wave["plan_s"], "init": "Gaussian pulse (SURVEY.md §8d)",
-                       "replay": wave["replay"], "execution": wave["execution"]},
-            "e2e": wave["e2e"], "roofline": wave["roofline"], "cpu_baseline": cpu,
-            "clocks": wave["clocks"], "gpu_launches": wave["gpu_launches"],
-            "energy": {"wave5": wave["energy"],
-                       "clock_sweep": clock_sweep(args, dist, placement) if args.energy else None},
-            "kernels": kernels,
-        }
+        sweep = clock_sweep(args, dist, placement) if args.energy else None
+        line = headline_line(args, dist.world, wave, cpu, kernels, sweep)
         print(json.dumps(line))
     if dist.world > 1:
         E.shutdown_distributed()

@@ -143,7 +143,6 @@ int cq_nccl_group_end(void);
 int cq_nccl_send(int device, int stream, const void* buf, int64_t bytes, int peer);
 int cq_nccl_recv(int device, int stream, void* buf, int64_t bytes, int peer);
 int cq_nccl_allgather(int device, int stream, const void* send, void* recv, int64_t bytes_per_rank);
-int cq_nccl_allreduce_max_f64(int device, int stream, double* buf, int64_t count);
 int cq_nccl_destroy(void);
 
 /* ----------------------------------------------------------------- kernels */
@@ -185,6 +184,12 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
                            const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
                            int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4,
                            const float* amax_in, float* amax_out);
+
+/* Geometry of one fused pass over `rows` output rows of a W-column grid:
+ * out = {rows per block, grid x, grid y, cells computed per level by the
+ * launched warps (halo columns / rows included)}.  Host-side query for the
+ * roofline's recompute share (bench.py); launches nothing. */
+int cq_wave5_fused_geometry(int device, int kind, int levels, int64_t rows, int64_t W, int64_t out[4]);
 
 /* Device interpreter for arbitrary task bodies (eval_kernel, kernel.py:291-331
  * with ReadView clamping + mapper check, model.py:442-453). */
@@ -239,6 +244,18 @@ int cq_error_flag_async(int device, int stream, void* host32);
  * vel_in).  The j order is fixed and independent of i_lo / the GPU count. */
 int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const float* vel_in,
                   float* vel, int64_t i_lo, int64_t i_hi, float eps2, float dt);
+/* The kick in pieces, so the j range already on the GPU is computed while
+ * the rest is still arriving (an 'all' mapper's all-gather, reference
+ * model.py:197-206): j is cut into cq_nbody_jcols() fixed columns, column c
+ * = bodies [floor(n c / C), floor(n (c+1) / C)).  kick_partial writes the
+ * per-body partial sums of columns [col_lo, col_hi) into part
+ * ([C][i_hi - i_lo][3] floats); kick_finalize adds the C columns in column
+ * order to vel_in.  Any split of the columns gives cq_nbody_kick's bits. */
+int cq_nbody_jcols(int* cols);
+int cq_nbody_kick_partial(int device, int stream, const float* pos, int64_t n, float* part, int64_t i_lo,
+                          int64_t i_hi, float eps2, int col_lo, int col_hi);
+int cq_nbody_kick_finalize(int device, int stream, const float* part, const float* vel_in, float* vel,
+                           int64_t count, float dt);
 /* p_i.xyz += dt * v_i.xyz for `count` bodies (p may alias p_in). */
 int cq_nbody_drift(int device, int stream, const float* p_in, const float* v, float* p,
                    int64_t count, float dt);

@@ -103,12 +103,15 @@ def nbody_accel_idx(pos, idx, eps2):
     return acc
 
 
-def sgemm_rows(a, b, rows):
+def sgemm_rows(a, b, rows, with_abs=True):
+    """float64 C rows (and sum |a||b| per element unless ``with_abs`` is
+    False, then None)."""
     a = np.ascontiguousarray(a, dtype=np.float32)
     b = np.ascontiguousarray(b, dtype=np.float32)
     rows = np.ascontiguousarray(rows, dtype=np.int64)
     n = b.shape[1]
     c = np.empty((rows.size, n), np.float64)
-    cabs = np.empty((rows.size, n), np.float64)
-    lib().oracle_sgemm_rows(_p(a), _p(b), n, a.shape[1], _p(rows), rows.size, _p(c), _p(cabs))
+    cabs = np.empty((rows.size, n), np.float64) if with_abs else None
+    lib().oracle_sgemm_rows(_p(a), _p(b), n, a.shape[1], _p(rows), rows.size, _p(c),
+                            _p(cabs) if with_abs else None)
     return c, cabs

@@ -98,7 +98,6 @@ _SIGS = {
     "cq_nccl_send": (i32, [i32, i32, vp, i64, i32]),
     "cq_nccl_recv": (i32, [i32, i32, vp, i64, i32]),
     "cq_nccl_allgather": (i32, [i32, i32, vp, vp, i64]),
-    "cq_nccl_allreduce_max_f64": (i32, [i32, i32, vp, i64]),
     "cq_nccl_destroy": (i32, []),
     "cq_fill": (i32, [i32, i32, i32, P(CqView), P(CqBox), P(CqBox), i32, ctypes.c_double, i64]),
     "cq_saxpy": (i32, [i32, i32, i32, ctypes.c_double, i64, vp, vp, vp, i64]),
@@ -109,11 +108,15 @@ _SIGS = {
     "cq_wave5_fused_bounded": (i32, [i32, i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqView), i64, i64,
                                      i64, i64, P(CqBox), ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      vp, vp]),
+    "cq_wave5_fused_geometry": (i32, [i32, i32, i32, i64, i64, P(i64)]),
     "cq_expr_eval": (i32, [i32, i32, P(CqExpr)]),
     "cq_error_flag": (i32, [i32, P(i32), P(i64), i32]),
     "cq_error_flag_async": (i32, [i32, i32, vp]),
     "cq_nbody_kick": (i32, [i32, i32, vp, i64, vp, vp, i64, i64, ctypes.c_float, ctypes.c_float]),
     "cq_nbody_drift": (i32, [i32, i32, vp, vp, vp, i64, ctypes.c_float]),
+    "cq_nbody_jcols": (i32, [P(i32)]),
+    "cq_nbody_kick_partial": (i32, [i32, i32, vp, i64, vp, i64, i64, ctypes.c_float, i32, i32]),
+    "cq_nbody_kick_finalize": (i32, [i32, i32, vp, vp, vp, i64, ctypes.c_float]),
     "cq_sgemm": (i32, [i32, i32, i32, vp, i64, vp, i64, vp, i64, i64, i64, i64]),
     "cq_jit_compile": (i32, [ctypes.c_char_p, ctypes.c_char_p, i32, P(ctypes.c_char_p),
                              P(ctypes.c_char_p), P(u64)]),

@@ -413,10 +413,10 @@ __device__ __forceinline__ void nb_interact2(f32x2 pix, f32x2 piy, f32x2 piz, f3
 
 // NP = i-body pairs per lane (independent FFMA2 chains); a block covers
 // 64*NP i-bodies.
-// The j range [0, n) is cut into NB_JCOLS * NB_WARPS fixed slices: block
-// column y (blockIdx.y) owns NB_WARPS consecutive slices, one per warp.
+// The j range [0, n) is cut into NB_JCOLS * NB_WARPS fixed slices: j column
+// c = col0 + blockIdx.y owns NB_WARPS consecutive slices, one per warp.
 // Each block writes its per-body partial (sum over its warps, fixed order)
-// to part_out[y]; nbody_kick_finalize sums the columns in fixed order and
+// to part_out[c]; nbody_kick_finalize sums the columns in fixed order and
 // applies the kick.  The slicing depends only on n, never on the i range,
 // so a body's acceleration is bit-identical for any GPU count, and the extra
 // grid dimension keeps every SM busy when each GPU owns few i-bodies.
@@ -425,7 +425,8 @@ constexpr int NB_JCOLS = 8;
 template <int NP>
 __global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4* __restrict__ pos,
                                                                    int64_t n, float* __restrict__ part_out,
-                                                                   int64_t i_lo, int64_t i_hi, float eps2) {
+                                                                   int64_t i_lo, int64_t i_hi, float eps2,
+                                                                   int col0) {
   constexpr int NB_IBLOCK = 64 * NP;
   // j tile, each body duplicated for the packed lanes: (x,x,y,y), (z,z,m,m)
   __shared__ __align__(16) float4 tile[NB_WARPS][32][2];
@@ -444,7 +445,8 @@ __global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4*
     ax[p] = ay[p] = az[p] = 0ull;
   }
   const f32x2 e2 = pack2(eps2, eps2);
-  const int64_t slice = (int64_t)blockIdx.y * NB_WARPS + warp;
+  const int col = col0 + blockIdx.y;  // j column of this block
+  const int64_t slice = (int64_t)col * NB_WARPS + warp;
   constexpr int64_t kSlices = (int64_t)NB_JCOLS * NB_WARPS;
   const int64_t jb = (n * slice) / kSlices, je = (n * (slice + 1)) / kSlices;
   float4 next = (jb + lane < je) ? pos[jb + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(NB_WARPS * 32) nbody_kick_kernel(const float4*
         sy += part[w][1][t];
         sz += part[w][2][t];
       }
-      float* o = part_out + ((int64_t)blockIdx.y * count + (i - i_lo)) * 3;
+      float* o = part_out + ((int64_t)col * count + (i - i_lo)) * 3;
       o[0] = sx;
       o[1] = sy;
       o[2] = sz;
@@ -542,7 +544,7 @@ __global__ void nbody_drift_kernel(const float4* p_in, const float4* __restrict_
 // A warp owns a strip of 32*V loaded columns (lane = V columns) and emits
 // the middle 32*V - 2*KL: level j is exact on columns [j, 32V-j) of the
 // strip (west/east neighbours by shuffle; the strip edge loses one column per
-// level).  It marches RB output rows, loading rows [r0-KL, r1+KL) of the
+// level).  It marches a piece of rows [r0, r1), loading rows [r0-KL, r1+KL) of the
 // inputs, keeping a 3-row window per level in registers (slot = row mod 3)
 // and a D-row prefetch ring (loop unrolled by lcm so every slot index is
 // static).  Global borders clamp exactly like the DSL's ReadView (the border
@@ -703,95 +705,123 @@ __device__ __forceinline__ void cp_async_wait() {
 // (cp.async, one commit group per row, each lane fetches and later reads
 // back only its own V columns), so D rows of both inputs are in flight per
 // warp without holding them in registers.
-// The register-heavy KL = 8, V = 4 variant runs one 12-warp block per SM:
-// with 32-bit row counters and running prefetch pointers it needs ~153
-// registers, under the 168 that 3 warps per SM sub-partition allow (the
-// earlier 64-bit row arithmetic needed ~200 and capped it at 8 warps;
-// 12 warps then spilled, profiles/r01/fused_cfg_sweep.log).  16 warps
-// (128 registers) spill 72 bytes a thread and measured 11% slower
-// (profiles/r01/w16_ab.log).  Other shapes run 8-warp blocks.
+// Warps per SM (one-warp blocks): the register-heavy KL = 8, V = 4 variant
+// runs 12 -- with 32-bit row counters and running prefetch pointers it fits
+// the 168 registers that 3 warps per SM sub-partition allow (64-bit row
+// arithmetic needed ~200 and capped it at 8; 16 warps at 128 registers
+// spill 72 bytes a thread and measured 11% slower, profiles/r01/w16_ab.log);
+// the other KL = 8 shapes 8, KL = 4 runs 16.  (Keeping the rows two iterations old of every
+// level in shared memory freed ~32 registers but measured slower: 16.7 vs
+// 20.8 TB/s, the extra LDS/STS per level cost more than the occupancy
+// gained.)
 template <int KL, int V>
 struct FusedShape {
-  // kOldInSmem keeps the rows two iterations old of every level in shared
-  // memory (each is read once more, as the north neighbour one level up and
-  // as u_prev two levels up), freeing ~32 registers: for KL = 8, V = 4 that
-  // fitted two 6-warp blocks per SM without spills when the kernel needed
-  // ~200 registers, but measured slower (16.7 vs 20.8 TB/s: the extra
-  // LDS/STS per level cost more than the 12 warps gained); the register-only
-  // kernel now reaches 12 warps per SM by itself (see above).
-  static constexpr bool kOldInSmem = false;
-  static constexpr int kWarps = (KL == 8 && V == 4) ? 12 : 8;
-  static constexpr int kMinBlocks = KL == 8 ? 1 : 2;
+  static constexpr int kWarpsPerSm = KL == 8 ? (V == 4 ? 12 : 8) : 16;
 };
 
-template <typename T, int KL, int V, int D, int RB>
-__global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL, V>::kMinBlocks)
+// Work split.  The pass's work is the output rows [out_lo, out_hi) of every
+// column strip, laid out strip-major (strip 0's rows, then strip 1's, ...)
+// and cut into ranges of `per_warp` rows; range q is the one-warp block q.
+// One-warp blocks keep every per-range quantity (rows, phases, store
+// windows) block-uniform, so ptxas proves the warp converged at each
+// shuffle (with a warp index from threadIdx the hot loop carried two
+// divergence checks per row); the block scheduler spreads consecutive
+// ranges -- and with them the slower column-border strips and row-border
+// pieces -- over the SMs.  A range that crosses a strip end is two pieces.  Each
+// piece marches its rows plus 2*KL halo rows in three phases of whole ring
+// turns: full border checks where a level meets row 0 / H-1 or a prefetch
+// leaves [in_lo, in_hi) (first / last turns of border pieces), column
+// checks only for strips touching column 0 / W-1, and the unchecked body
+// (FMA form when the previous pass bounded |X|, else the exact form).
+// One balanced range per warp slot (launch_fused) replaces the earlier 2-D
+// grid of 224-row segments: no half-empty last wave and no partial last
+// block column of 3 busy warps out of 12, and 2*KL halo rows per ~1365
+// rows instead of per 224 (16384^2: 13 x 74 blocks = 6.5 waves -> 147
+// blocks, one per SM).
+// march modes (bit flags): row-border checks, column-border checks, FMA form
+enum { kRows = 1, kCols = 2, kFast = 4, kEdgeAll = kRows | kCols };
+
+template <typename T, int KL, int V, int D, int WPB>
+__global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB)
     wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last, cq_view_t out_prev, int64_t in_lo,
-                       int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c, T k2, T k4,
-                       int64_t seg, const float* __restrict__ amax_in, float* __restrict__ amax_out, float limit) {
+                       int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c,
+                       int64_t per_warp, int map, const float* __restrict__ amax_in,
+                       float* __restrict__ amax_out, float limit) {
   typedef typename FVec<T, V>::T Vec;
   static_assert(KL >= 2 && KL % V == 0, "strip offsets must stay vector aligned");
   static_assert(D % 3 == 0, "prefetch ring must be a multiple of the window");
   constexpr int SW = 32 * V - 2 * KL;
   extern __shared__ __align__(16) uint8_t fused_smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr bool OLD_SM = FusedShape<KL, V>::kOldInSmem;
-  constexpr int WPB_ = FusedShape<KL, V>::kWarps;
-  Vec* ring = reinterpret_cast<Vec*>(fused_smem) + (size_t)warp * D * 2 * 32;  // [D][2][32]
-  // [KL][3][32] per warp after all rings: level j's rows by slot (OLD_SM only)
-  Vec* olds = reinterpret_cast<Vec*>(fused_smem) + (size_t)WPB_ * D * 2 * 32 + (size_t)warp * KL * 3 * 32;
-  const int64_t strip = (int64_t)blockIdx.x * FusedShape<KL, V>::kWarps + warp;
-  const int64_t r0 = out_lo + (int64_t)blockIdx.y * seg;  // seg output rows per block (launch_fused)
-  if (strip * SW >= W || r0 >= out_hi) return;  // warp-uniform
-  const int64_t r1 = min(r0 + seg, out_hi);
-  const int64_t c0 = strip * SW - KL;  // first loaded column of the strip
-  const int64_t col = c0 + lane * V;
-  const bool colok = col >= 0 && col < W;
-  const bool keep = lane >= KL / V && lane < 32 - KL / V && col < W;
-  (void)k2;
-  (void)k4;  // 2 and 4 (host-checked): formed as exact sums in wave_pair
-  const int64_t rb = r0 - KL, re = r1 + KL;  // input rows this warp streams
-  // Almost every warp is interior: no border clamping, every input row
-  // readable.  Border strips / segments take the checked path.
-  // Decided per block (from blockIdx and parameters only), so the branch is
-  // CTA-uniform and the shuffles inside need no divergence fallback.
-  // (Per-warp decisions with warps walking (strip, segment) pairs on a 1-D
-  // grid -- no partial block columns -- measured 2% slower.)
-  constexpr int WPB = FusedShape<KL, V>::kWarps;
-  const int64_t bc0 = (int64_t)blockIdx.x * WPB * SW - KL;  // first loaded column of the block
-  const bool interior = bc0 > 0 && bc0 + (WPB - 1) * SW + 32 * V < W && rb - KL > 0 && re < H && rb >= in_lo &&
-                        re <= in_hi;
+  const int lane = threadIdx.x & 31, warp = WPB == 1 ? 0 : threadIdx.x >> 5;
+  Vec* ring = reinterpret_cast<Vec*>(fused_smem) + (size_t)warp * D * 2 * 32;  // [D][2][32] per warp
+  const int64_t rows = out_hi - out_lo;
+  const int64_t strips = (W + SW - 1) / SW, total = strips * rows;
+  const int64_t q = map == 1 ? (int64_t)warp * gridDim.x + blockIdx.x : (int64_t)blockIdx.x * WPB + warp;
+  int64_t p, pend;
+  if (map == 2) {
+    // strip-minor: range q is strip q % strips, piece q / strips
+    const int64_t st = q % strips, a0 = q / strips * per_warp;
+    p = st * rows + a0;
+    pend = a0 < rows ? st * rows + min(rows, a0 + per_warp) : p;
+  } else {
+    p = q * per_warp;
+    pend = min(p + per_warp, total);
+  }
   // |inputs| bound from the previous pass (amax_in, null: unknown); NaN
   // compares false and keeps the exact form
-  const bool fast = interior && amax_in != nullptr && *amax_in < limit;
+  const bool fast = p < pend && amax_in != nullptr && *amax_in < limit;
   float amax = 0.f;  // max |stored value| of this warp (amax_out)
   const int64_t us = u.stride[1], ps = upr.stride[1];
-  const T* ub = (const T*)u.ptr + (colok ? col : 0) - u.alloc.lo[2] + (rb - u.alloc.lo[1]) * us;
-  const T* pb = (const T*)upr.ptr + (colok ? col : 0) - upr.alloc.lo[2] + (rb - upr.alloc.lo[1]) * ps;
-  T* sl = (T*)out_last.ptr + (col - out_last.alloc.lo[2]) + (r0 - out_last.alloc.lo[1]) * out_last.stride[1];
-  T* sp = (T*)out_prev.ptr + (col - out_prev.alloc.lo[2]) + (r0 - out_prev.alloc.lo[1]) * out_prev.stride[1];
   const int64_t ls = out_last.stride[1], pstr = out_prev.stride[1];
 
-  // rows are counted from rb in 32-bit (t = ri - rb); the store windows in
-  // t: out_prev (level KL-1, row rb + t - KL + 1 in [r0, r1)) and out_last
-  // (level KL, row rb + t - KL >= r0; always < r1)
-  const int nrow = (int)(re - rb);
-  const int prev_lo = 2 * KL - 1, prev_hi = (int)(r1 - rb) + KL - 1, last_lo = 2 * KL;
+  while (p < pend) {  // warp-uniform
+    const int64_t strip = p / rows;
+    const int64_t a = p - strip * rows, b = min(rows, a + (pend - p));
+    p += b - a;
+    const int64_t r0 = out_lo + a, r1 = out_lo + b;
+    const int64_t c0 = strip * SW - KL;  // first loaded column of the strip
+    const int64_t col = c0 + lane * V;
+    const bool colok = col >= 0 && col < W;
+    const bool keep = lane >= KL / V && lane < 32 - KL / V && col < W;
+    const int64_t rb = r0 - KL, re = r1 + KL;  // input rows this piece streams
+    const T* ub = (const T*)u.ptr + (colok ? col : 0) - u.alloc.lo[2] + (rb - u.alloc.lo[1]) * us;
+    const T* pb = (const T*)upr.ptr + (colok ? col : 0) - upr.alloc.lo[2] + (rb - upr.alloc.lo[1]) * ps;
+    T* sl = (T*)out_last.ptr + (col - out_last.alloc.lo[2]) + (r0 - out_last.alloc.lo[1]) * ls;
+    T* sp = (T*)out_prev.ptr + (col - out_prev.alloc.lo[2]) + (r0 - out_prev.alloc.lo[1]) * pstr;
+    // rows are counted from rb in 32-bit (t = ri - rb); the store windows in
+    // t: out_prev (level KL-1, row rb + t - KL + 1 in [r0, r1)) and out_last
+    // (level KL, row rb + t - KL >= r0; always < r1)
+    const int nrow = (int)(re - rb);
+    const int prev_lo = 2 * KL - 1, prev_hi = (int)(r1 - rb) + KL - 1, last_lo = 2 * KL;
+    // phases (whole ring turns): iterations t < t1 see row 0 (t <= KL - rb)
+    // or prefetch below in_lo; t >= t2 see row H-1 (t >= H - rb) or
+    // prefetch at / above in_hi (only when re > in_hi)
+    const int nfull = nrow / D * D;
+    int64_t top = in_lo - rb - D, bot = H - rb;
+    if (KL - rb + 1 > top) top = KL - rb + 1;
+    if (top < 0) top = 0;
+    if (nrow < bot) bot = nrow;
+    if (re > in_hi && in_hi - rb - D < bot) bot = in_hi - rb - D;
+    if (bot < 0) bot = 0;
+    const int t1 = (int)(top >= nfull ? nfull : (top + D - 1) / D * D);
+    int t2 = (int)(bot >= nfull ? nfull : bot / D * D);
+    if (t2 < t1) t2 = t1;
+    const bool col_edge = !(c0 > 0 && c0 + 32 * V < W);
 
-  auto march = [&](auto edge_tag, auto fast_tag) {
-    constexpr bool EDGE = decltype(edge_tag)::value;
-    constexpr bool FAST = decltype(fast_tag)::value;
     // running source pointers of the next row to prefetch (row rb + t + D)
     const T* uf = ub + (int64_t)D * us;
     const T* pf = pb + (int64_t)D * ps;
     // fetch input row rb + k into ring slot `slot` from (uk, pk)
-    auto fetch = [&](int slot, int k, const T* uk, const T* pk) {
+    auto fetch = [&](auto mode, int slot, int k, const T* uk, const T* pk) {
+      constexpr int M = decltype(mode)::value;
       bool ok = true;
-      if (EDGE) {
+      if (M & kRows) {
         const int64_t r = rb + k;
         ok = colok && r >= in_lo && r < in_hi;
-        if (!ok) uk = ub, pk = pb;  // any mapped address; zero-filled, not read
+      } else if (M & kCols) {
+        ok = colok;
       }
+      if (!ok) uk = ub, pk = pb;  // any mapped address; zero-filled, not read
       cp_async_row(ring + (slot * 2 + 0) * 32 + lane, uk, ok, sizeof(Vec));
       cp_async_row(ring + (slot * 2 + 1) * 32 + lane, pk, ok, sizeof(Vec));
     };
@@ -799,41 +829,38 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
     Vec P[3];      // X(t-1) rows, same slots
 #pragma unroll
     for (int q = 0; q < D; ++q) {
-      if (q < nrow) fetch(q, q, ub + (int64_t)q * us, pb + (int64_t)q * ps);
+      if (q < nrow) fetch(std::integral_constant<int, kEdgeAll>{}, q, q, ub + (int64_t)q * us, pb + (int64_t)q * ps);
       cp_async_commit();
     }
     // one input row: land it, prefetch row t + D, advance every level
-    auto row = [&](const int t, const int sd) {
+    auto row = [&](auto mode, const int t, const int sd) {
+      constexpr int M = decltype(mode)::value;
       const int s = sd % 3, so = (sd + 1) % 3, sm = (sd + 2) % 3;  // rows t, t-2, t-1
       cp_async_wait<D - 1>();  // row t (the oldest group) has landed
       L[0][s] = ring[(sd * 2 + 0) * 32 + lane];
       P[s] = ring[(sd * 2 + 1) * 32 + lane];
-      if (OLD_SM) olds[(0 * 3 + s) * 32 + lane] = L[0][s];
-      if (t + D < nrow) fetch(sd, t + D, uf, pf);
+      if (t + D < nrow) fetch(mode, sd, t + D, uf, pf);
       cp_async_commit();
       uf += us;
       pf += ps;
-      // the row two iterations old of level k (north of level k+1, u_prev of k+2)
-      auto old_of = [&](int k) -> Vec { return OLD_SM ? olds[(k * 3 + so) * 32 + lane] : L[k][so]; };
 #pragma unroll
       for (int j = 1; j <= KL; ++j) {
         const Vec mid = L[j - 1][sm];
-        Vec nn = old_of(j - 1), ss = L[j - 1][s];
+        Vec nn = L[j - 1][so], ss = L[j - 1][s];
         T wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
         T ev = __shfl_down_sync(0xffffffffu, first_of(mid), 1);
-        if (EDGE) {
+        if (M & kRows) {
           const int64_t rho = rb + t - j;
           if (rho == 0) nn = mid;
           if (rho == H - 1) ss = mid;
+        }
+        if (M & kCols) {
           if (col == 0) wv = first_of(mid);
           if (col + V == W) ev = last_of(mid);
         }
-        const Vec pp = (j == 1) ? P[sm] : old_of(j >= 2 ? j - 2 : 0);
-        const Vec o = FAST ? wave_vec_fast(mid, nn, ss, pp, wv, ev, c) : wave_vec(mid, nn, ss, pp, wv, ev, c);
-        if (j < KL) {
-          L[j][s] = o;
-          if (OLD_SM) olds[(j * 3 + s) * 32 + lane] = o;
-        }
+        const Vec pp = (j == 1) ? P[sm] : L[j >= 2 ? j - 2 : 0][so];
+        const Vec o = (M & kFast) ? wave_vec_fast(mid, nn, ss, pp, wv, ev, c) : wave_vec(mid, nn, ss, pp, wv, ev, c);
+        if (j < KL) L[j][s] = o;
         if (j == KL - 1 && t >= prev_lo && t < prev_hi) {
           if (keep) {
             __stcs(reinterpret_cast<Vec*>(sp), o);
@@ -852,20 +879,28 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
     };
     // whole ring turns without a bounds test (the warp stays converged, so
     // the shuffles need no collective fallback), then the remainder
-    int base = 0;
+    auto turns = [&](auto mode, int& t, const int end) {
 #pragma unroll 1
-    for (; base + D <= nrow; base += D) {
+      for (; t < end; t += D) {
 #pragma unroll
-      for (int sd = 0; sd < D; ++sd) row(base + sd, sd);
+        for (int sd = 0; sd < D; ++sd) row(mode, t + sd, sd);
+      }
+    };
+    int t = 0;
+    turns(std::integral_constant<int, kEdgeAll>{}, t, t1);
+    if (col_edge) {
+      if (fast) turns(std::integral_constant<int, kCols | kFast>{}, t, t2);
+      else turns(std::integral_constant<int, kCols>{}, t, t2);
+    } else {
+      if (fast) turns(std::integral_constant<int, kFast>{}, t, t2);
+      else turns(std::integral_constant<int, 0>{}, t, t2);
     }
+    turns(std::integral_constant<int, kEdgeAll>{}, t, nfull);
 #pragma unroll
     for (int sd = 0; sd < D; ++sd)
-      if (base + sd < nrow) row(base + sd, sd);
-  };
-  if (fast) march(std::false_type{}, std::true_type{});
-  else if (interior) march(std::false_type{}, std::false_type{});
-  else march(std::true_type{}, std::false_type{});
-  cp_async_wait<0>();
+      if (nfull + sd < nrow) row(std::integral_constant<int, kEdgeAll>{}, nfull + sd, sd);
+    cp_async_wait<0>();
+  }
   if (amax_out != nullptr) {
     // values are >= 0, so their int bit patterns order like the floats
 #pragma unroll
@@ -874,50 +909,34 @@ __global__ void __launch_bounds__(32 * FusedShape<KL, V>::kWarps, FusedShape<KL,
   }
 }
 
-// Rows per block.  A block marches its rows plus 2*KL halo rows, and one
-// KL = 8 block fills an SM.  A fixed segment is wrong on short slabs (a
-// node's slab at high node counts, a strong-scaled run): 512 rows x 19 strip
-// groups of 256 rows is 38 blocks for 148 SMs.  Rule, from a sweep of 6
-// slab heights x 9 segments (profiles/r01/fused_seg_sweep.log, seg_check.log):
-// * tall slabs (>= 4 waves of blocks at the cap): the cap, 224 rows for
-//   KL = 8 (longer segments measured slower even at equal work: 16384 rows,
-//   529 rows 1.17 ms vs 224 rows 1.03 ms);
-// * otherwise pick the number of waves w and the longest segment <= cap that
-//   fills them, minimising (w + 1/4) * (seg + 2 KL) (the quarter block is the
-//   tail of the slowest, border block): 512 rows run in 0.059 ms instead of
-//   0.168 ms;
-// * KL = 4 (two blocks per SM) was fastest at 32 rows at every height.
-// CQ_FUSED_SEG=<rows> forces a fixed segment.
-static int64_t fused_segment(int64_t rows, int64_t gx, int64_t slots, int kl, int64_t cap) {
-  const char* env = getenv("CQ_FUSED_SEG");  // read per launch (sweeps set it between launches)
-  const int64_t forced = env ? (int64_t)atoll(env) : 0;
-  if (forced > 0) return forced;
-  auto blocks_for = [&](int64_t seg) { return gx * ((rows + seg - 1) / seg); };
-  if (slots <= 0 || blocks_for(cap) >= 4 * slots) return cap;
-  int64_t best = cap;
-  double best_cost = 1e300;
-  for (int64_t w = 1; w <= 64; ++w) {
-    const int64_t ny = (w * slots) / gx;
-    if (ny < 1) continue;
-    const int64_t seg = std::min(cap, std::max<int64_t>(32, (rows + ny - 1) / ny));
-    const int64_t waves = (blocks_for(seg) + slots - 1) / slots;
-    const double cost = ((double)waves + 0.25) * (double)(seg + 2 * kl);
-    if (cost < best_cost) best_cost = cost, best = seg;
-    if (seg == 32) break;
-  }
-  return best;
+// Launch geometry of one fused pass over output rows [out_lo, out_lo + rows)
+// of a W-column grid: rows per warp range, the grid, and the cells the
+// launched warps compute per level (strip width x marched rows, halo
+// columns / rows and dead lanes included) -- the denominator of the pass's
+// recompute share (bench.py's roofline).
+//
+// Rows per warp range: one block per SM slot and, when the strips divide
+// the warp slots well (>= 95% busy), k = slots / strips ranges per strip of
+// ceil(rows / k) rows (no range crosses a strip end: 16384^2 at KL = 8 is 147
+// strips x 12 ranges of 1366 rows for 1776 warp slots); otherwise an equal
+// share of the strip-major row space.  The 4-step pass is HBM-bound and kept
+// the short ranges it measured fastest with (32 rows, as the earlier 2-D
+// grid's segments).  CQ_FUSED_ROWS=<rows> forces the range length.
+struct FusedGeometry {
+  int64_t per_warp, blocks, warps, computed_cells;
+  int smem, threads, map;
+};
+
+static int fused_map() {
+  const char* e = getenv("CQ_FUSED_MAP");  // read per launch (A/B sweeps)
+  return e ? atoi(e) : 2;
 }
 
-template <typename T, int KL, int V, int D, int RB>
-static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& upr, const cq_view_t& ol,
-                        const cq_view_t& op, int64_t in_lo, int64_t in_hi, int64_t out_lo, int64_t out_hi,
-                        int64_t H, int64_t W, T c, T k2, T k4, const float* amax_in, float* amax_out,
-                        float limit) {
+template <typename T, int KL, int V, int D, int WPB>
+static int fused_geometry(int64_t rows, int64_t W, FusedGeometry* g) {
   constexpr int sw = 32 * V - 2 * KL;
-  const int64_t strips = (W + sw - 1) / sw;
-  constexpr int WPB = FusedShape<KL, V>::kWarps;
-  auto kern = wave5_fused_kernel<T, KL, V, D, RB>;
-  const int smem = WPB * (D * 2 + (FusedShape<KL, V>::kOldInSmem ? KL * 3 : 0)) * 32 * V * (int)sizeof(T);
+  auto kern = wave5_fused_kernel<T, KL, V, D, WPB>;
+  const int smem = WPB * D * 2 * 32 * V * (int)sizeof(T);
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   // resident blocks per SM of this instantiation (same on every B200)
   static const int per_sm = [&] {
@@ -927,12 +946,112 @@ static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& up
   int dev = 0, sms = 0;
   CQ_CHECK_CUDA(cudaGetDevice(&dev));
   CQ_CHECK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t gx = (strips + WPB - 1) / WPB, rows = out_hi - out_lo;
-  const int64_t seg = fused_segment(rows, gx, (int64_t)per_sm * sms, KL, std::min<int64_t>(RB, KL == 8 ? 224 : 32));
-  dim3 grid((unsigned)gx, (unsigned)((rows + seg - 1) / seg));
-  kern<<<grid, 32 * WPB, smem, st>>>(u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, seg, amax_in,
-                                     amax_out, limit);
+  const int64_t strips = (W + sw - 1) / sw, total = strips * rows;
+  const int64_t slots = std::max<int64_t>(1, (int64_t)per_sm * sms) * WPB;
+  g->map = fused_map();
+  const char* env = getenv("CQ_FUSED_ROWS");  // read per launch (sweeps set it between launches)
+  const int64_t forced = env ? (int64_t)atoll(env) : 0;
+  int64_t per;
+  if (forced > 0) {
+    per = forced;
+  } else {
+    // short pieces (profiles/r02 sweeps), shorter still when a launch would
+    // not fill the warp slots
+    const int64_t cap = KL == 8 ? 224 : 32, floor_rows = KL == 8 ? 16 : 8;
+    per = std::min(cap, std::max(floor_rows, (total + slots - 1) / slots));
+  }
+  per = std::max<int64_t>(1, per);
+  g->per_warp = per;
+  const int64_t pieces = (rows + per - 1) / per;
+  g->warps = g->map == 2 ? strips * pieces : (total + per - 1) / per;
+  g->blocks = (g->warps + WPB - 1) / WPB;
+  // every piece marches its rows + 2 KL halo rows over 32 V columns
+  int64_t marched = 0;
+  if (g->map == 2) {
+    marched = strips * (rows + 2 * KL * pieces);
+  } else {
+    for (int64_t q = 0; q < g->warps; ++q) {
+      for (int64_t p = q * per, e = std::min(p + per, total); p < e;) {
+        const int64_t a = p % rows, b = std::min(rows, a + (e - p));
+        marched += b - a + 2 * KL;
+        p += b - a;
+      }
+    }
+  }
+  g->computed_cells = marched * 32 * V;
+  g->smem = smem;
+  g->threads = 32 * WPB;
   return CQ_OK;
+}
+
+template <typename T, int KL, int V, int D, int WPB>
+static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& upr, const cq_view_t& ol,
+                        const cq_view_t& op, int64_t in_lo, int64_t in_hi, int64_t out_lo, int64_t out_hi,
+                        int64_t H, int64_t W, T c, const float* amax_in, float* amax_out, float limit) {
+  FusedGeometry g;
+  CQ_TRY((fused_geometry<T, KL, V, D, WPB>(out_hi - out_lo, W, &g)));
+  wave5_fused_kernel<T, KL, V, D, WPB><<<(unsigned)g.blocks, g.threads, g.smem, st>>>(
+      u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, g.per_warp, g.map, amax_in, amax_out, limit);
+  return CQ_OK;
+}
+
+// One fused pass: its launch parameters, or (geometry != null) only the
+// geometry it would launch with.
+struct FusedLaunch {
+  cudaStream_t st;
+  const cq_view_t *u, *upr, *out_last, *out_prev;
+  int64_t in_lo, in_hi, out_lo, out_hi, H, W;
+  double c, k2, k4;
+  const float* amax_in;
+  float* amax_out;
+  float limit;
+  FusedGeometry* geometry;
+};
+
+template <typename T, int KL, int V, int D, int WPB = 1>
+static int fused_run(const FusedLaunch& L) {
+  if (L.geometry) return fused_geometry<T, KL, V, D, WPB>(L.out_hi - L.out_lo, L.W, L.geometry);
+  return launch_fused<T, KL, V, D, WPB>(L.st, *L.u, *L.upr, *L.out_last, *L.out_prev, L.in_lo, L.in_hi, L.out_lo,
+                                        L.out_hi, L.H, L.W, (T)L.c, L.amax_in, L.amax_out, L.limit);
+}
+
+// warps per block: CQ_FUSED_WPB (A/B sweeps; 1 = one-warp blocks)
+static int fused_wpb() {
+  const char* e = getenv("CQ_FUSED_WPB");
+  return e ? atoi(e) : 1;
+}
+
+// tuning: CQ_WAVE_FUSED_CFG="V,D" (lane width, cp.async ring depth);
+// default 4,6 (KL = 4: two 8-warp blocks / SM; KL = 8: one 12-warp block /
+// SM, its 8 levels of register windows need ~153 registers)
+static int fused_dispatch(int kind, int levels, const FusedLaunch& L) {
+  if (kind == CQ_F64) {
+    // two doubles per lane (16-byte rows): 56 (KL = 4) or 48 (KL = 8) valid
+    // columns per warp strip
+    return levels == 4 ? fused_run<double, 4, 2, 6>(L) : fused_run<double, 8, 2, 6>(L);
+  }
+  static int cfg_env = [] {
+    int v = 0, d = 0;
+    if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d", &v, &d);
+    return v ? v * 100 + d : 0;
+  }();
+  const int cfg = cfg_env ? cfg_env : 4 * 100 + 6;
+  switch (cfg * 10 + levels) {
+#define CQ_FUSED_CASE(VV, DD, KL) \
+  case (VV * 100 + DD) * 10 + KL: \
+    return fused_run<float, KL, VV, DD>(L);
+    case (4 * 100 + 6) * 10 + 4:
+      return fused_wpb() == 8 ? fused_run<float, 4, 4, 6, 8>(L) : fused_run<float, 4, 4, 6>(L);
+    case (4 * 100 + 6) * 10 + 8:
+      return fused_wpb() == 12 ? fused_run<float, 8, 4, 6, 12>(L) : fused_run<float, 8, 4, 6>(L);
+    CQ_FUSED_CASE(4, 9, 4) CQ_FUSED_CASE(4, 9, 8)
+    CQ_FUSED_CASE(4, 12, 4) CQ_FUSED_CASE(4, 12, 8)
+    CQ_FUSED_CASE(2, 12, 4) CQ_FUSED_CASE(2, 12, 8)
+#undef CQ_FUSED_CASE
+    default:
+      set_error("cq_wave5_fused: CQ_WAVE_FUSED_CFG=%d not compiled", cfg);
+      return CQ_ERR_ARG;
+  }
 }
 
 }  // namespace cq
@@ -1059,16 +1178,6 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
   CQ_REQUIRE(out_lo >= lo_ok && out_hi <= hi_ok && in_lo >= 0 && in_hi <= H,
              "cq_wave5_fused: rows [%lld, %lld) are not determined by input rows [%lld, %lld)",
              (long long)out_lo, (long long)out_hi, (long long)in_lo, (long long)in_hi);
-  // tuning: CQ_WAVE_FUSED_CFG="V,D,RB" (lane width, cp.async ring depth,
-  // upper bound on rows per block, see fused_segment); default 4,6,128 for
-  // KL = 4 (two 8-warp blocks / SM) and 4,6,256 for KL = 8 (one 12-warp
-  // block / SM: its 8 levels of register windows need ~153 registers)
-  static int cfg_env = [] {
-    int v = 0, d = 0, rb = 0;
-    if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d,%d", &v, &d, &rb);
-    return v ? v * 10000 + d * 1000 + rb : 0;
-  }();
-  const int cfg = cfg_env ? cfg_env : (levels == 8 ? 4 * 10000 + 6 * 1000 + 256 : 4 * 10000 + 6 * 1000 + 128);
   // the fast form is exact while every value of the pass stays below 2^125
   // (then 2u and 4u do not overflow); one step grows max|X| by at most
   // g = 3 + 8|c| (|2u| + |p| + |c| |n+s+w+e-4u|), so inputs below
@@ -1078,39 +1187,30 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
     return !(e && e[0] == '0');
   }();
   const float limit = fast_ok ? (float)(std::ldexp(1.0, 124) / std::pow(3.0 + 8.0 * std::fabs(c) + 1e-3, levels)) : 0.f;
-  int status;
-  if (kind == CQ_F64) {
-    // two doubles per lane (16-byte rows): 56 (KL = 4) or 48 (KL = 8) valid
-    // columns per warp strip
-    if (levels == 4)
-      status = launch_fused<double, 4, 2, 6, 128>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi,
-                                                  H, W, c, k2, k4, amax_in, amax_out, limit);
-    else
-      status = launch_fused<double, 8, 2, 6, 256>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi,
-                                                  H, W, c, k2, k4, amax_in, amax_out, limit);
-    if (status != CQ_OK) return status;
-    CQ_CHECK_LAUNCH();
-    return CQ_OK;
-  }
-  switch (cfg * 10 + levels) {
-#define CQ_FUSED_CASE(VV, DD, RBB, KL)                                                               \
-  case (VV * 10000 + DD * 1000 + RBB) * 10 + KL:                                                   \
-    status = launch_fused<float, KL, VV, DD, RBB>(st, *u, *upr, *out_last, *out_prev, in_lo, in_hi, out_lo, out_hi, \
-                                                  H, W, (float)c, (float)k2, (float)k4, amax_in, amax_out, limit); \
-    break;
-    CQ_FUSED_CASE(4, 6, 128, 4) CQ_FUSED_CASE(4, 6, 128, 8)
-    CQ_FUSED_CASE(4, 6, 256, 4) CQ_FUSED_CASE(4, 6, 256, 8)
-    CQ_FUSED_CASE(4, 9, 256, 4) CQ_FUSED_CASE(4, 9, 256, 8)
-    CQ_FUSED_CASE(4, 12, 128, 4) CQ_FUSED_CASE(4, 12, 128, 8)
-    CQ_FUSED_CASE(4, 12, 256, 4) CQ_FUSED_CASE(4, 12, 256, 8)
-    CQ_FUSED_CASE(2, 12, 128, 4) CQ_FUSED_CASE(2, 12, 128, 8)
-#undef CQ_FUSED_CASE
-    default:
-      set_error("cq_wave5_fused: CQ_WAVE_FUSED_CFG=%d not compiled", cfg);
-      return CQ_ERR_ARG;
-  }
-  if (status != CQ_OK) return status;
+  FusedLaunch L{st, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, amax_in, amax_out,
+                limit, nullptr};
+  CQ_TRY(fused_dispatch(kind, levels, L));
   CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_wave5_fused_geometry(int device, int kind, int levels, int64_t rows, int64_t W, int64_t out[4]) {
+  CQ_TRY(ensure_device(device));
+  CQ_CHECK_CUDA(cudaSetDevice(device));
+  CQ_REQUIRE(levels == 4 || levels == 8, "cq_wave5_fused_geometry: levels must be 4 or 8 (got %d)", levels);
+  CQ_REQUIRE(kind == CQ_F32 || kind == CQ_F64, "cq_wave5_fused_geometry: float kinds only");
+  CQ_REQUIRE(rows > 0 && W > 0, "cq_wave5_fused_geometry: empty launch");
+  FusedGeometry g;
+  FusedLaunch L{};
+  L.out_lo = 0;
+  L.out_hi = rows;
+  L.W = W;
+  L.geometry = &g;
+  CQ_TRY(fused_dispatch(kind, levels, L));
+  out[0] = g.per_warp;
+  out[1] = g.blocks;
+  out[2] = g.warps;
+  out[3] = g.computed_cells;
   return CQ_OK;
 }
 
@@ -1155,10 +1255,8 @@ int cq_error_flag_async(int device, int stream, void* host32) {
   return CQ_OK;
 }
 
-int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const float* vel_in,
-                  float* vel, int64_t i_lo, int64_t i_hi, float eps2, float dt) {
-  CQ_GET_STREAM(device, stream);
-  if (i_hi <= i_lo) return CQ_OK;
+static int nbody_partial(cudaStream_t st, const float* pos, int64_t n, float* part, int64_t i_lo, int64_t i_hi,
+                         float eps2, int col_lo, int col_hi) {
   static int forced = [] {
     const char* e = getenv("CQ_NBODY_NP");
     return e ? atoi(e) : 0;
@@ -1168,13 +1266,11 @@ int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const flo
   // widest variant (4 pairs per lane, best steady-state rate) fills the GPU
   // even at 32768 bodies per GPU; CQ_NBODY_NP overrides for experiments.
   const int use = forced ? forced : 4;
-  float* part = nullptr;
-  CQ_TRY(scratch(device, stream, 1, (size_t)NB_JCOLS * bodies * 3 * sizeof(float), (void**)&part));
   switch (use) {
-#define NB_LAUNCH(P)                                                                                 \
-  case P:                                                                                          \
-    nbody_kick_kernel<P><<<dim3((unsigned)((bodies + 64 * P - 1) / (64 * P)), NB_JCOLS), NB_WARPS * 32, 0, \
-                           st>>>((const float4*)pos, n, part, i_lo, i_hi, eps2);                  \
+#define NB_LAUNCH(P)                                                                                        \
+  case P:                                                                                                 \
+    nbody_kick_kernel<P><<<dim3((unsigned)((bodies + 64 * P - 1) / (64 * P)), col_hi - col_lo), NB_WARPS * 32, 0, \
+                           st>>>((const float4*)pos, n, part, i_lo, i_hi, eps2, col_lo);                \
     break;
     NB_LAUNCH(1)
     NB_LAUNCH(2)
@@ -1184,8 +1280,43 @@ int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const flo
 #undef NB_LAUNCH
   }
   CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_nbody_kick(int device, int stream, const float* pos, int64_t n, const float* vel_in,
+                  float* vel, int64_t i_lo, int64_t i_hi, float eps2, float dt) {
+  CQ_GET_STREAM(device, stream);
+  if (i_hi <= i_lo) return CQ_OK;
+  const int64_t bodies = i_hi - i_lo;
+  float* part = nullptr;
+  CQ_TRY(scratch(device, stream, 1, (size_t)NB_JCOLS * bodies * 3 * sizeof(float), (void**)&part));
+  CQ_TRY(nbody_partial(st, pos, n, part, i_lo, i_hi, eps2, 0, NB_JCOLS));
   nbody_kick_finalize<<<grid_for(bodies, 256, ds->sm_count, 8), 256, 0, st>>>(
       part, (const float4*)vel_in, (float4*)vel, bodies, dt);
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_nbody_jcols(int* cols) {
+  *cols = NB_JCOLS;
+  return CQ_OK;
+}
+
+int cq_nbody_kick_partial(int device, int stream, const float* pos, int64_t n, float* part, int64_t i_lo,
+                          int64_t i_hi, float eps2, int col_lo, int col_hi) {
+  CQ_GET_STREAM(device, stream);
+  CQ_REQUIRE(0 <= col_lo && col_lo <= col_hi && col_hi <= NB_JCOLS, "cq_nbody_kick_partial: columns [%d, %d) "
+             "outside [0, %d)", col_lo, col_hi, NB_JCOLS);
+  if (i_hi <= i_lo || col_hi == col_lo) return CQ_OK;
+  return nbody_partial(st, pos, n, part, i_lo, i_hi, eps2, col_lo, col_hi);
+}
+
+int cq_nbody_kick_finalize(int device, int stream, const float* part, const float* vel_in, float* vel,
+                           int64_t count, float dt) {
+  CQ_GET_STREAM(device, stream);
+  if (count <= 0) return CQ_OK;
+  nbody_kick_finalize<<<grid_for(count, 256, ds->sm_count, 8), 256, 0, st>>>(
+      part, (const float4*)vel_in, (float4*)vel, count, dt);
   CQ_CHECK_LAUNCH();
   return CQ_OK;
 }

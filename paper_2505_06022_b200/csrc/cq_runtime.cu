@@ -76,24 +76,51 @@ cudaStream_t stream_of(int device, int stream) {
   return d->streams[stream];
 }
 
+// Per (device, stream, slot) scratch that only grows.  A grown-out block is
+// retired, not freed: queued work or an already captured CUDA graph may
+// still reference it (freeing it would need a stream synchronize, illegal
+// while capturing, and would still break the graph); retired blocks are
+// freed by cq_shutdown after a device synchronize.  Growth during a capture
+// is refused -- the run before the capture sizes every scratch.
 static std::map<std::tuple<int, int, int>, std::pair<void*, size_t>> g_scratch;
+static std::vector<std::pair<int, void*>> g_retired;
 
 int scratch(int device, int stream, int slot, size_t bytes, void** ptr) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto& e = g_scratch[std::make_tuple(device, stream, slot)];
   if (e.second < bytes) {
-    if (e.first) {
-      // growing: the old block may still be in use by queued work
-      CQ_CHECK_CUDA(cudaStreamSynchronize(stream_of(device, stream)));
-      CQ_CHECK_CUDA(cudaFree(e.first));
-      e.first = nullptr;
-      e.second = 0;
-    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CQ_CHECK_CUDA(cudaStreamIsCapturing(stream_of(device, stream), &cap));
+    CQ_REQUIRE(cap == cudaStreamCaptureStatusNone,
+               "scratch: growing slot %d to %zu bytes while capturing a CUDA graph (run the plan once "
+               "before capturing it)", slot, bytes);
+    if (e.first) g_retired.emplace_back(device, e.first);
+    e.first = nullptr;
+    e.second = 0;
     CQ_CHECK_CUDA(cudaMalloc(&e.first, bytes));
     e.second = bytes;
   }
   *ptr = e.first;
   return CQ_OK;
+}
+
+static void free_scratch(int device) {
+  for (auto it = g_scratch.begin(); it != g_scratch.end();) {
+    if (std::get<0>(it->first) == device) {
+      cudaFree(it->second.first);
+      it = g_scratch.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  for (auto it = g_retired.begin(); it != g_retired.end();) {
+    if (it->first == device) {
+      cudaFree(it->second);
+      it = g_retired.erase(it);
+    } else {
+      ++it;
+    }
+  }
 }
 
 // ------------------------------------------------------------- memory pool
@@ -171,6 +198,7 @@ int cq_shutdown(void) {
     cudaDeviceSynchronize();
     for (auto& kv : g_pool[i].free_blocks) cudaFree(kv.second);
     g_pool[i].free_blocks.clear();
+    free_scratch(i);
     for (int s = 0; s < CQ_NUM_STREAMS; ++s) cudaStreamDestroy(g_dev[i].streams[s]);
     cudaFree(g_dev[i].error_flag);
     g_dev[i] = DeviceState();
@@ -593,13 +621,6 @@ int cq_nccl_allgather(int device, int stream, const void* send, void* recv, int6
   CQ_STREAM(device, stream);
   CQ_REQUIRE(g_comm && device == g_comm_device, "NCCL not initialised for device %d", device);
   CQ_CHECK_NCCL(ncclAllGather(send, recv, (size_t)bytes_per_rank, ncclChar, g_comm, st));
-  return CQ_OK;
-}
-
-int cq_nccl_allreduce_max_f64(int device, int stream, double* buf, int64_t count) {
-  CQ_STREAM(device, stream);
-  CQ_REQUIRE(g_comm && device == g_comm_device, "NCCL not initialised for device %d", device);
-  CQ_CHECK_NCCL(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclMax, g_comm, st));
   return CQ_OK;
 }
 

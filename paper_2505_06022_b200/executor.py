@@ -33,6 +33,7 @@ and a send and its receive are always posted in the same group.
 import ctypes
 import heapq
 import os
+import weakref
 from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import Optional
@@ -186,7 +187,12 @@ def shutdown_distributed():
 
 # ---------------------------------------------------------------- host memory
 
-_pinned = {}   # (start, end) byte span -> owning array (kept alive)
+# Page-locked spans of host arrays: (start, end) -> weakref.finalize that
+# unregisters the span when the array owning the memory is garbage-collected
+# (so registrations live exactly as long as the arrays, and repeated runs
+# over the same inputs register them once), or a strong reference for memory
+# no ndarray owns.
+_pinned = {}
 _temp_spans = set()
 _PAGE = 4096
 # Only arrays this large are page-locked: glibc serves them from their own
@@ -231,10 +237,28 @@ def _raise_flag(code, point):
         raise MapperViolationError(f"read at id {point} outside the mapped region")
 
 
+def _memory_owner(arr):
+    """The ndarray that owns ``arr``'s memory (walking view bases), or None."""
+    o = arr
+    while isinstance(o, np.ndarray) and o.base is not None:
+        o = o.base
+    return o if isinstance(o, np.ndarray) and o.base is None else None
+
+
+def _unregister_span(span):
+    if _pinned.pop(span, None) is not None:
+        try:
+            N.call("cq_host_unregister", ctypes.c_void_p(span[0]))
+        except Exception:  # noqa: BLE001  (interpreter shutdown / library gone)
+            pass
+
+
 def _pin_span(arr: np.ndarray, box=None, keep=True):
     """Page-lock the bytes of a large ``arr`` spanning ``box`` (whole array if
     None); a rank of a weak-scaled run pins only its own rows of a big host
-    array.  Returns the span when registered temporarily (keep=False)."""
+    array.  keep=True: the registration lasts until the array owning the
+    memory is garbage-collected (or ``release_pinned``).  Returns the span
+    when registered temporarily (keep=False)."""
     if arr.nbytes < PIN_MIN_BYTES:
         return None
     a, b = _byte_span(arr, box)
@@ -244,7 +268,13 @@ def _pin_span(arr: np.ndarray, box=None, keep=True):
         return None
     N.call("cq_host_register", ctypes.c_void_p(start), end - start)
     if keep:
-        _pinned[(start, end)] = arr
+        owner = _memory_owner(arr)
+        if owner is not None:
+            fin = weakref.finalize(owner, _unregister_span, (start, end))
+            fin.atexit = False
+            _pinned[(start, end)] = fin
+        else:
+            _pinned[(start, end)] = arr
         return None
     _temp_spans.add((start, end))
     return (start, end)
@@ -266,9 +296,13 @@ def _pin(arr: np.ndarray):
 
 
 def release_pinned():
-    for (start, _end), _a in list(_pinned.items()):
-        N.call("cq_host_unregister", ctypes.c_void_p(start))
-    _pinned.clear()
+    """Unregister every kept registration now (they otherwise end with
+    their arrays)."""
+    for span, holder in list(_pinned.items()):
+        if isinstance(holder, weakref.finalize):
+            holder.detach()
+        _pinned.pop(span, None)
+        N.call("cq_host_unregister", ctypes.c_void_p(span[0]))
 
 
 def pinned_empty(shape, dtype, box=None) -> np.ndarray:
@@ -446,6 +480,7 @@ class Session:
         self._raw = None        # the plan's schedule before fusion (schedule())
         self._lanes = None      # node -> compute stream (lane())
         self._exec_of = None    # (task id, node) -> ExecuteCommand (exec_fused)
+        self._jcols = None      # N-body j columns (cq_nbody_jcols)
         self._halo_marks = []   # trace marks of a fused block's halo transfers
         self.t0 = None
         self._t0 = {}
@@ -672,7 +707,13 @@ class Session:
             elif src_l or dst_l:
                 nccl_ops.append(push)
         if nccl_ops:
-            self.nccl_group(nccl_ops)
+            # the 'all' exchange is recognised on the whole group (identical
+            # on every rank), then this rank's part of it posted
+            layout = self._allgather_layout([p for p in group if p.deps])
+            if layout is not None:
+                self.allgather(nccl_ops, *layout)
+            else:
+                self.nccl_group(nccl_ops)
 
     def local_copy(self, push):
         src = self.views[(push.src, push.buffer)]
@@ -687,6 +728,52 @@ class Session:
                 N.call("cq_copy_box", dev, N.STREAM_COMM, eb, ctypes.byref(dst.c), dst.device,
                        ctypes.byref(src.c), src.device, ctypes.byref(cb))
         self.mark_transfer(push, push.dst, self.issue(dev, N.STREAM_COMM, acc, go))
+
+    def _allgather_layout(self, pushes):
+        """(buffer, rows per rank) when ``pushes`` are an 'all' mapper's full
+        exchange (reference model.py:197-206): every node sends its equal
+        dim-0 slab of one buffer to every other node, node k being rank k and
+        each rank holding the whole buffer -- then one in-place
+        ncclAllGather replaces the G(G-1) sends and receives."""
+        G = self.nodes
+        if self.pl.world < 2 or G != self.pl.world or len(pushes) != G * (G - 1):
+            return None
+        buf = pushes[0].buffer
+        ext = self.buffers[buf].extent
+        S, rem = divmod(ext.maxs[0], G)
+        if rem or any(p.buffer != buf for p in pushes):
+            return None
+        if {(p.src, p.dst) for p in pushes} != {(a, b) for a in range(G) for b in range(G) if a != b}:
+            return None
+        for p in pushes:
+            if len(p.region.boxes) != 1 or self.rank(p.src) != p.src:
+                return None
+            b = p.region.boxes[0]
+            if b.mins != (p.src * S,) + ext.mins[1:] or b.maxs != ((p.src + 1) * S,) + ext.maxs[1:]:
+                return None
+        v = self.views.get((self.pl.rank, buf))
+        if v is None or v.box != ext:
+            return None
+        return buf, S
+
+    def allgather(self, pushes, buf, rows):
+        """One in-place all-gather of ``buf``'s slabs on the comm stream."""
+        dev = self.pl.devices[0]
+        me = self.pl.rank
+        v = self.views[(me, buf)]
+        ext = self.buffers[buf].extent
+        row_bytes = v.nbytes // ext.maxs[0]
+        mine = Region.from_box(Box((me * rows,) + ext.mins[1:], ((me + 1) * rows,) + ext.maxs[1:]))
+        others = Region.from_box(ext).difference(mine)
+        acc = [(me, buf, mine, False), (me, buf, others, True)]
+
+        def go():
+            N.call("cq_nccl_allgather", dev, N.STREAM_COMM, ctypes.c_void_p(v.addr((me * rows,) + ext.mins[1:])),
+                   ctypes.c_void_p(v.ptr), rows * row_bytes)
+        t = self.issue(dev, N.STREAM_COMM, acc, go)
+        for p in pushes:
+            if self.local(p.src) or self.local(p.dst):
+                self.mark_transfer(p, p.src if self.local(p.src) else p.dst, t)
 
     def nccl_group(self, pushes):
         """Sends and receives of this rank, posted as one NCCL group."""
@@ -807,6 +894,11 @@ class Session:
             self.issue(dev, lane, [(node, buf, reg, False)], go)
             rviews[name] = snap
 
+        if binding.kind == "native" and binding.args["name"] == "nbody.kick":
+            pos_buf = next(a.buffer for a in task.accessors if a.name == "pos")
+            if pos_buf in awaited:
+                self.exec_kick(task, cmd, binding, awaited[pos_buf], dev, lane, rviews, wviews)
+                return
         pieces = self.split(task, cmd, awaited)
         marks = []
         for box, dependent in pieces:
@@ -897,6 +989,62 @@ class Session:
             if self.want_trace:
                 for i, tid in enumerate(block.tasks):
                     self.trace_marks.append((self._exec_of[(tid, node)], node, dev, marks, (i, kl)))
+
+    def exec_kick(self, task, cmd, binding, got, dev, lane, rviews, wviews):
+        """The N-body kick of a chunk whose 'all'-mapped positions are partly
+        still arriving (``got``: the awaited region): the j columns already
+        held (cq_nbody_jcols fixed columns) run at once on the compute lane,
+        the others on the boundary stream once their slabs land, and the
+        finalize adds every column in column order -- the bits of one
+        cq_nbody_kick, for any GPU count (reference model.py:197-206)."""
+        node = cmd.node
+        pos_buf = next(a.buffer for a in task.accessors if a.name == "pos")
+        vbuf = next(a.buffer for a in task.accessors if a.name == "vel")
+        n = self.buffers[pos_buf].extent.maxs[0]
+        width = self.buffers[pos_buf].extent.maxs[1]
+        if self._jcols is None:
+            c = ctypes.c_int32()
+            N.call("cq_nbody_jcols", ctypes.byref(c))
+            self._jcols = c.value
+        C = self._jcols
+        box = cmd.chunk.box
+        lo, hi = box.mins[0], box.maxs[0]
+        runs = []   # (col_lo, col_hi, waits for the awaited slabs)
+        for c in range(C):
+            cols = Region.from_box(Box((n * c // C, 0), (n * (c + 1) // C, width)))
+            remote = cols.overlaps(got)
+            if runs and runs[-1][2] == remote and runs[-1][1] == c:
+                runs[-1][1] = c + 1
+            else:
+                runs.append([c, c + 1, remote])
+        runs.sort(key=lambda r: r[2])   # held columns first
+        part = self.scratch_alloc(dev, C * (hi - lo) * 3 * 4)
+        pkey = f"__kick_part_{part:x}"
+        pos, vin, vout = rviews["pos"], rviews["vel_in"], wviews["vel"]
+        eps2, dt = task.params["eps2"], task.params["dt"]
+        marks = []
+        for c0, c1, remote in runs:
+            stream = N.STREAM_BOUNDARY if remote else lane
+            reads = Region.from_box(Box((n * c0 // C, 0), (n * c1 // C, width)))
+            acc = [(node, pos_buf, reads, False), (node, pkey, Region.from_box(Box((c0,), (c1,))), True)]
+
+            def go(c0=c0, c1=c1, stream=stream):
+                N.call("cq_nbody_kick_partial", dev, stream, ctypes.c_void_p(pos.addr((0, 0))), n,
+                       ctypes.c_void_p(part), lo, hi, ctypes.c_float(eps2), c0, c1)
+            t = self.issue(dev, stream, acc, go)
+            marks.append(t)
+            if self.want_trace:
+                self.launch_log.append(("nbody.kick", box.volume() * (c1 - c0) // C, dev, stream, t[0], t[1]))
+        vreg = Region.from_box(box)
+        acc = [(node, pkey, Region.from_box(Box((0,), (C,))), False), (node, vbuf, vreg, False),
+               (node, vbuf, vreg, True)]
+
+        def fin():
+            N.call("cq_nbody_kick_finalize", dev, lane, ctypes.c_void_p(part), ctypes.c_void_p(vin.addr((lo, 0))),
+                   ctypes.c_void_p(vout.addr((lo, 0))), hi - lo, ctypes.c_float(dt))
+        marks.append(self.issue(dev, lane, acc, fin))
+        if self.want_trace:
+            self.trace_marks.append((cmd, node, dev, marks, None))
 
     def split(self, task, cmd, awaited):
         """Cut the chunk along dim 0 into rows that do not read awaited
@@ -1207,6 +1355,9 @@ class Session:
         self._drop_graph()
         saved = self.want_trace
         graphs, logs, events, scratch = [], [], [], []
+        # a fused block swaps the current / alternate allocations as it is
+        # issued; a capture failing part-way must not leave any swap behind
+        views0, alt0 = dict(self.views), dict(self.alt)
         try:
             for _k in range(2 if self._odd_chains() else 1):
                 self.want_trace = timed
@@ -1243,8 +1394,10 @@ class Session:
             _free_scratch(scratch)
             for ev in events:
                 N.call("cq_event_destroy", ctypes.c_uint64(ev))
-            if len(graphs) % 2:   # one capture's view swaps without its partner
-                self._toggle_odd_chains()
+            self.views.clear()
+            self.views.update(views0)
+            self.alt.clear()
+            self.alt.update(alt0)
             self.recycle()
             raise
         # capturing executed nothing: with two graphs the views are back where
@@ -1336,6 +1489,14 @@ class Session:
         self._t0 = {}
 
     def close(self):
+        # work queued on the allocations (an exception path of run /
+        # run_batch) must finish before they return to the pool
+        for d in self.devices:
+            for st in N.ALL_STREAMS:
+                try:
+                    N.call("cq_stream_synchronize", d, st)
+                except NativeError:
+                    pass
         self._drop_graph()
         self.release()
         if self._flag_host is not None:

@@ -20,10 +20,12 @@ What changes against executing the plan command by command: the plan's
 one-row halo pushes of the fused tasks are replaced by one KL-row exchange
 per block; the last task's pushes are still posted after the chain, so every
 halo row the plan's ``final_locations`` lists holds its final version.
-Chains run KL = 8 blocks (half the bytes per step of KL = 4) with KL = 4
-blocks where the parity needs them: an even number of out-of-place
-blocks keeps the current allocations where a CUDA-graph capture found them;
-leftover steps (< 4) run one step at a time.
+Chains run as many KL = 8 blocks as fit (half the bytes per step of KL = 4)
+and one KL = 4 block, placed first, for a remaining quarter (``_blocks``;
+100 steps = 1 x KL4 + 12 x KL8).  An odd number of out-of-place blocks
+leaves a run's fields in the alternate allocations: the executor follows
+them, and a CUDA-graph capture records two alternating graphs
+(``Session.capture``).  Leftover steps (< 4) run one step at a time.
 
 ``CQ_WAVE_FUSE=0`` disables the transformation.
 """

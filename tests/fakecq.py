@@ -214,11 +214,11 @@ class FakeLib:
         self.group.append(("recv", _val(buf), int(_val(n)), int(_val(peer))))
         return 0
 
-    def cq_nccl_allgather(self, *a):
-        return N.CQ_ERR_UNSUPPORTED
-
-    def cq_nccl_allreduce_max_f64(self, *a):
-        return N.CQ_ERR_UNSUPPORTED
+    def cq_nccl_allgather(self, d, s, send, recv, n):
+        """In-place ncclAllGather semantics over the transport."""
+        self.transport.allgather(self, _val(send), _val(recv), int(_val(n)))
+        self.launches.append(("allgather", int(_val(n))))
+        return 0
 
     def cq_nccl_destroy(self):
         return 0
@@ -404,17 +404,46 @@ class FakeLib:
             self.flag = None
         return 0
 
-    def cq_nbody_kick(self, d, s, pos, n, vin, vout, lo, hi, eps2, dt_):
-        n, lo, hi = int(_val(n)), int(_val(lo)), int(_val(hi))
+    NB_JCOLS = 8
+
+    def cq_nbody_jcols(self, p):
+        _obj(p).value = self.NB_JCOLS
+        return 0
+
+    def cq_nbody_kick_partial(self, d, s, pos, n, part, lo, hi, eps2, c0, c1):
+        """Per-column partial accelerations (float64 sums rounded once) --
+        the structure, not the bits, of the GPU kernel."""
+        n, lo, hi, c0, c1 = (int(_val(x)) for x in (n, lo, hi, c0, c1))
+        C = self.NB_JCOLS
         P = self._arr(_val(pos), [n, 4], [4, 1], np.float32).astype(np.float64)
-        vi = self._arr(_val(vin), [hi - lo, 4], [4, 1], np.float32)
-        vo = self._arr(_val(vout), [hi - lo, 4], [4, 1], np.float32)
-        d3 = P[None, :, :3] - P[lo:hi, None, :3]
-        r2 = (d3 ** 2).sum(-1) + _val(eps2)
-        a = (d3 * (P[None, :, 3] / r2 ** 1.5)[..., None]).sum(1)
+        out = self._arr(_val(part), [C, hi - lo, 3], [(hi - lo) * 3, 3, 1], np.float32)
+        for c in range(c0, c1):
+            jb, je = n * c // C, n * (c + 1) // C
+            d3 = P[None, jb:je, :3] - P[lo:hi, None, :3]
+            r2 = (d3 ** 2).sum(-1) + _val(eps2)
+            out[c] = (d3 * (P[None, jb:je, 3] / r2 ** 1.5)[..., None]).sum(1).astype(np.float32)
+        self.launches.append("nbody.partial")
+        return 0
+
+    def cq_nbody_kick_finalize(self, d, s, part, vin, vout, count, dt_):
+        count = int(_val(count))
+        C = self.NB_JCOLS
+        pa = self._arr(_val(part), [C, count, 3], [count * 3, 3, 1], np.float32)
+        acc = np.zeros((count, 3), np.float32)
+        for c in range(C):
+            acc += pa[c]
+        vi = self._arr(_val(vin), [count, 4], [4, 1], np.float32)
         res = vi.copy()
-        res[:, :3] += (_val(dt_) * a).astype(np.float32)
-        vo[...] = res
+        res[:, :3] += np.float32(_val(dt_)) * acc
+        self._arr(_val(vout), [count, 4], [4, 1], np.float32)[...] = res
+        return 0
+
+    def cq_nbody_kick(self, d, s, pos, n, vin, vout, lo, hi, eps2, dt_):
+        lo, hi = int(_val(lo)), int(_val(hi))
+        part = np.zeros((self.NB_JCOLS, hi - lo, 3), np.float32)
+        addr = part.ctypes.data
+        self.cq_nbody_kick_partial(d, s, pos, n, addr, lo, hi, eps2, 0, self.NB_JCOLS)
+        self.cq_nbody_kick_finalize(d, s, addr, vin, vout, hi - lo, dt_)
         return 0
 
     def cq_nbody_drift(self, d, s, pin, v, pout, count, dt_):
@@ -515,6 +544,9 @@ class LocalTransport:
         if ops:
             raise AssertionError("NCCL op issued in a single-process run")
 
+    def allgather(self, lib, send, recv, n):
+        raise AssertionError("NCCL all-gather issued in a single-process run")
+
 
 class GlooTransport:
     """NCCL group semantics over torch.distributed (gloo): all sends and
@@ -539,6 +571,17 @@ class GlooTransport:
         for addr, n, t in recvs:
             lib._mem(addr, n)[:] = t.numpy()
         lib.launches.append(("group", len(ops)))
+
+    def allgather(self, lib, send, recv, n):
+        import torch
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(), dist.get_rank()
+        assert send == recv + rank * n, "all-gather must be in place (rank r's chunk at recv + r * n)"
+        t = torch.from_numpy(lib._mem(send, n).copy())
+        out = [torch.empty(n, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(out, t)
+        for r, o in enumerate(out):
+            lib._mem(recv + r * n, n)[:] = o.numpy()
 
 
 def _graph_api(cls):
@@ -566,7 +609,8 @@ def _graph_api(cls):
     cls.cq_graph_launch, cls.cq_graph_destroy = launch, destroy
     # wrap kernel entry points so they are recorded while capturing
     for name in ("cq_saxpy", "cq_wave5", "cq_wave5_fused", "cq_expr_eval", "cq_fill", "cq_copy_box", "cq_pack_box",
-                 "cq_unpack_box", "cq_nbody_kick", "cq_nbody_drift", "cq_sgemm"):
+                 "cq_unpack_box", "cq_nbody_kick", "cq_nbody_drift", "cq_sgemm", "cq_nbody_kick_partial",
+                 "cq_nbody_kick_finalize"):
         fn = getattr(cls, name)
 
         def wrapped(self, *args, _fn=fn, _name=name):

@@ -196,3 +196,48 @@ def to_reference(buffers, tasks):
         rtasks.append(r.Task(name=t.name, global_range=box(t.global_range), accessors=accs,
                              body=body, params=dict(t.params), beta=t.beta, target=tgt))
     return rbufs, rtasks
+
+
+def to_reference_plan(plan, rgraph):
+    """This package's ``Plan`` as the reference's command objects over the
+    reference graph ``rgraph`` (built from the same program, so task ids
+    agree), for the reference's own ``check_plan`` (tests/helpers.py:59-165)."""
+    r = ref()
+    rs = sys.modules["clusterq.scheduler"]
+
+    def box(b):
+        return r.Box(b.mins, b.maxs)
+
+    def region(g):
+        return r.Region(g.dims, [box(b) for b in g.boxes])
+
+    cmds = []
+    for c in plan.commands:
+        kind = type(c).__name__
+        if kind == "ExecuteCommand":
+            cmds.append(rs.ExecuteCommand(c.id, tuple(c.deps), rs.Chunk(c.chunk.task_id, box(c.chunk.box),
+                                                                          c.chunk.node),
+                                          c.frequency_ghz, tuple((a, b, region(g)) for a, b, g in c.reads),
+                                          tuple((a, b, region(g), v) for a, b, g, v in c.writes)))
+        elif kind == "PushCommand":
+            cmds.append(rs.PushCommand(c.id, tuple(c.deps), c.src, c.dst, c.buffer, region(c.region), c.version))
+        else:
+            cmds.append(rs.AwaitPushCommand(c.id, tuple(c.deps), c.dst, c.buffer, region(c.region), c.version,
+                                            c.push_id))
+    finals = {name: [(region(g), v, set(h)) for g, v, h in entries]
+              for name, entries in plan.final_locations.items()}
+    return rs.Plan(rgraph, plan.node_count, cmds, [], r.EnergyTarget.MAX_PERF, finals)
+
+
+def drop_push(plan, push):
+    """``plan`` without ``push`` and its AwaitPush (and the deps on them) --
+    the negative control: a plan that loses one transfer."""
+    import dataclasses
+    gone = {push.id} | {c.id for c in plan.commands
+                        if type(c).__name__ == "AwaitPushCommand" and c.push_id == push.id}
+    cmds = []
+    for c in plan.commands:
+        if c.id in gone:
+            continue
+        cmds.append(dataclasses.replace(c, deps=tuple(d for d in c.deps if d not in gone)))
+    return dataclasses.replace(plan, commands=cmds)

@@ -165,7 +165,14 @@ def _rank_main(rank, world, port, outdir):
     # N-body: the 'all' mapper's pushes = an all-gather group per step;
     # sgemm: A slabs scattered, B broadcast (host-init lowering at each rank)
     for nodes in (2, 3):
+        before = len(lib.launches)
         res = E.run(cq.generate_commands(_nbody_prog().graph(), nodes), placement=pl)
+        new = lib.launches[before:]
+        # 2 nodes = 2 ranks: one in-place all-gather per later step, and the
+        # kick split into held / arriving j columns
+        results[f"nbody{nodes}_allgathers_r{rank}"] = np.array(
+            [sum(1 for x in new if isinstance(x, tuple) and x[0] == "allgather"),
+             sum(1 for x in new if x == "nbody.partial")])
         if rank == 0:
             results[f"nbody{nodes}_P"], results[f"nbody{nodes}_V"] = res.buffers["P"], res.buffers["V"]
         res = E.run(cq.generate_commands(_sgemm_prog().graph(), nodes), placement=pl)
@@ -204,6 +211,10 @@ def test_two_ranks_gloo(tmp_path):
     single_nb = E.run(cq.generate_commands(_nbody_prog().graph(), 1), placement=E.Placement(1, 0, (0,)))
     single_mm = E.run(cq.generate_commands(_sgemm_prog().graph(), 1), placement=E.Placement(1, 0, (0,)))
     N._lib = None
+    for r in (r0, r1):
+        ag2, part2 = r[f"nbody2_allgathers_r{r is r1:d}"]
+        ag3, _ = r[f"nbody3_allgathers_r{r is r1:d}"]
+        assert ag2 == 1 and part2 >= 2 and ag3 == 0   # 3 nodes on 2 ranks: send/recv groups
     for nodes in (2, 3):
         assert dsl.same_bits(r0[f"nbody{nodes}_P"], single_nb.buffers["P"])
         assert dsl.same_bits(r0[f"nbody{nodes}_V"], single_nb.buffers["V"])
@@ -238,12 +249,48 @@ def test_graph_capture_replays_same_commands(fake):
     assert s.graph is None and s.graph_events == []
 
 
+def test_failed_capture_restores_fused_views(fake):
+    """A capture that fails part-way through a fused chain (here: the
+    second block's launch) leaves no current / alternate swap behind: the
+    stream replay that follows continues the simulation exactly."""
+    from oracle import native as onat
+    lib = fake(1)
+    h, w, steps = 288, 64, 20          # 3 out-of-place blocks: KL4 + 2 x KL8
+    u0 = np.random.default_rng(21).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=steps, kind="float32", u0=u0, up0=u0)
+    s = E.Session(cq.generate_commands(prog.graph(), 3), E.Placement(1, 0, (0,)))
+    assert [b.kl for b in s.chains[0].blocks] == [4, 8, 8]
+    s.execute(upload=True)
+    s.synchronize()
+    s.recycle()
+    real = lib.cq_wave5_fused_bounded
+    calls = []
+
+    def failing(*args):
+        if lib.capturing is not None:
+            calls.append(1)
+            if len(calls) == 4:        # block 2's first launch (3 nodes per block)
+                return N.CQ_ERR_ARG
+        return real(*args)
+    lib.cq_wave5_fused_bounded = failing
+    with pytest.raises(cq.NativeError):
+        s.capture()
+    lib.cq_wave5_fused_bounded = real
+    s.execute(upload=False)
+    s.synchronize()
+    res = s.results()
+    s.close()
+    u, up = onat.wave_run(u0, u0, 2 * steps, 0.25)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
 # ------------------------------------------- temporally blocked wave chains
 
 @pytest.mark.parametrize("steps,nodes,ndev", [(22, 1, 1), (22, 3, 1), (16, 4, 2), (9, 2, 1), (100, 3, 2)])
 def test_fused_wave_chain_matches_oracle(fake, monkeypatch, steps, nodes, ndev):
-    """Fused blocks (KL=4 and a parity KL=8 block) + plain leftovers give the
-    per-step result bit for bit, with nodes sharing or spanning devices."""
+    """Fused blocks (a KL=4 block for a remaining quarter first, then KL=8
+    blocks; odd block counts included) + plain leftovers give the per-step
+    result bit for bit, with nodes sharing or spanning devices."""
     from paper_2505_06022_b200 import fusion
     from oracle import native as onat
     lib = fake(ndev)
@@ -385,6 +432,41 @@ def test_partially_pinned_input_is_bounced_through_a_copy(fake, monkeypatch):
     from oracle import native as onat
     u, up = onat.wave_run(u0, u0, 2, 0.25)
     assert dsl.same_bits(res.buffers["u"], u)
+
+
+def test_input_registrations_end_with_their_arrays(fake):
+    """Page-locked input spans live as long as the arrays owning them:
+    repeated runs over one input register it once, and dropping the program
+    and its arrays unregisters it (no process-lifetime growth, run_batch over
+    fresh per-job inputs included)."""
+    import gc
+    lib = fake(1)
+    live = set()
+    reg, unreg = lib.cq_host_register, lib.cq_host_unregister
+    lib.cq_host_register = lambda p, n: live.add(_addr(p)) or reg(p, n)
+    lib.cq_host_unregister = lambda p: live.discard(_addr(p)) or unreg(p)
+    n = (E.PIN_MIN_BYTES // 8) + 1024
+    x = np.random.default_rng(3).uniform(-1, 1, n)
+    y = np.ones(n)
+    prog = W.saxpy_program(n, kind="float64", x=x, y=y)
+    plan = cq.generate_commands(prog.graph(), 2)
+    E.run(plan, placement=E.Placement(1, 0, (0,)), trace=False)
+    kept = dict(E._pinned)
+    assert len(kept) == 2 and live == {s for s, _e in kept}   # x and y; the result's span was temporary
+    E.run(plan, placement=E.Placement(1, 0, (0,)), trace=False)
+    assert E._pinned == kept                                   # registered once
+    jobs = [({"x": np.full(n, float(k)), "y": y}, None) for k in range(3)]
+    E.run_batch(plan, jobs, placement=E.Placement(1, 0, (0,)))
+    del jobs
+    gc.collect()
+    assert E._pinned == kept and live == {s for s, _e in kept}, "fresh per-job inputs must not stay registered"
+    del prog, plan, x, y, kept
+    gc.collect()
+    assert not E._pinned and not live
+
+
+def _addr(p):
+    return p.value if hasattr(p, "value") else int(p)
 
 
 def test_fused_wave_chain_float64(fake):

@@ -411,30 +411,41 @@ def test_trace_and_energy_accounting():
 
 def test_nbody_baseline_size_sampled():
     """BASELINE config 2 size: 262,144 bodies; 1,024 sampled i-bodies x all
-    j against the float64 oracle (SURVEY.md §8d tolerance 1e-4)."""
+    j against the float64 oracle (SURVEY.md §8d tolerance 1e-4), on 1 node
+    and on 8 nodes sharing the GPU (the 'all' mapper's all-gather between
+    them); the 8-node result is bit-identical to the 1-node one (fixed,
+    GPU-count independent j order)."""
     n, eps2, dt = 262144, 1e-2, 1e-3
     pos, vel = W.nbody_inputs(n)
     prog = W.nbody_program(n, steps=1, eps2=eps2, dt=dt, pos=pos, vel=vel)
-    res = run(cq.generate_commands(prog.graph(), 1))
     idx = np.random.default_rng(0).choice(n, 1024, replace=False)
-    got = res.buffers["V"][idx, :3].astype(np.float64) / dt
     want = onat.nbody_accel_idx(pos, idx, eps2)
-    err = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
-    assert err.max() <= 1e-4, err.max()
+    out = {}
+    for nodes in (1, 8):
+        res = run(cq.generate_commands(prog.graph(), nodes), trace=False)
+        got = res.buffers["V"][idx, :3].astype(np.float64) / dt
+        err = np.linalg.norm(got - want, axis=1) / np.linalg.norm(want, axis=1)
+        assert err.max() <= 1e-4, (nodes, err.max())
+        out[nodes] = res.buffers
+    for name in ("P", "V"):
+        assert dsl.same_bits(out[1][name], out[8][name]), name
 
 
 @pytest.mark.parametrize("variant", ["3xtf32", "ffma"])
 def test_sgemm_baseline_size_sampled(variant):
-    """BASELINE config 3 size: 16384^3 fp32; 256 sampled rows of C against a
-    float64 oracle, |C - C64| / sum|a||b| <= 1e-6."""
+    """BASELINE config 3 size: 16384^3 fp32 with slice mappers on 1 node and
+    on 8 nodes (2048-row A / C slabs, B everywhere); 256 sampled rows of C
+    against a float64 oracle, |C - C64| / sum|a||b| <= 1e-6."""
     m = 16384
     a, b = W.sgemm_inputs(m, m, m)
     prog = W.sgemm_program(m, m, m, variant=variant, a=a, b=b)
-    res = run(cq.generate_commands(prog.graph(), 1), trace=False)
     rows = np.random.default_rng(1).choice(m, 256, replace=False)
     c, cabs = onat.sgemm_rows(a, b, rows)
-    err = np.abs(res.buffers["C"][rows] - c) / cabs
-    assert err.max() <= 1e-6, err.max()
+    for nodes in (1, 8):
+        res = run(cq.generate_commands(prog.graph(), nodes), trace=False)
+        err = np.abs(res.buffers["C"][rows] - c) / cabs
+        assert err.max() <= 1e-6, (nodes, err.max())
+        del res
 
 
 @pytest.mark.parametrize("nodes", [1, 3])
@@ -487,14 +498,14 @@ def test_run_batch_two_in_flight_matches_oracle():
 
 def test_wave_baseline_size_bit_exact():
     """BASELINE config 1 at full size: 16384 x 16384 fp32, 100 steps,
-    temporally blocked (11 eight-step + 3 four-step passes) on one GPU and
-    on 4 nodes sharing it (KL-row halo exchanges between the slabs), against
-    the OpenMP oracle of the per-step tree -- bit for bit."""
+    temporally blocked (1 four-step + 12 eight-step passes) on one GPU and
+    on 4 and 8 nodes sharing it (KL-row halo exchanges between the slabs),
+    against the OpenMP oracle of the per-step tree -- bit for bit."""
     from paper_2505_06022_b200.executor import Placement, Session
     n, steps = 16384, 100
     u0 = W.wave_pulse(n, n, "float32")
     u, up = onat.wave_run(u0, u0, steps, 0.25)
-    for nodes in (1, 4):
+    for nodes in (1, 4, 8):
         prog = W.wave_program(n, n, steps=steps, kind="float32", c=0.25, u0=u0, up0=u0)
         s = Session(cq.generate_commands(prog.graph(), nodes), Placement(1, 0, (0,)), trace=False)
         assert [b.kl for b in s.chains[0].blocks] == [4] + [8] * 12

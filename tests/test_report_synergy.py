@@ -131,3 +131,17 @@ def test_bench_reference_arm_contract_line():
     assert d["impl"] == "reference" and d["warmup"] >= 3 and d["steps"] == 2
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] in ("port", "reference")
     assert d["value"] > 0 and d["cpu_baseline"]["value"] == d["value"]
+    # the driver pairs the arms by metric / unit / higher_is_better: the b200
+    # arm's line (headline_line) must carry the same strings and config
+    import types
+    sys.path.insert(0, root)
+    import bench
+    with open(os.path.join(root, "BASELINE.json")) as fh:
+        assert d["metric"] == json.load(fh)["metric"] == bench.METRIC
+    args = types.SimpleNamespace(size=256, steps=2, warmup=3, wave_steps=bench.WAVE_STEPS)
+    wave = {"value": 1.0, "ms_per_step": 1.0, "plan_s": 0.0, "replay": "cuda_graph", "execution": "",
+            "e2e": {}, "roofline": {}, "clocks": {}, "gpu_launches": 1, "energy": None}
+    mine = bench.headline_line(args, 1, wave, None, None, None)
+    for key in ("metric", "unit", "higher_is_better", "config", "scaling", "dtype", "n_gpus", "steps", "warmup"):
+        assert mine[key] == d[key], key
+    assert d["ms_per_step"] > 0 and "100 time steps per bench step" in d["config"]["workload"]
