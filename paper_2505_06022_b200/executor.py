@@ -33,6 +33,7 @@ and a send and its receive are always posted in the same group.
 import ctypes
 import heapq
 import os
+import time
 import weakref
 from dataclasses import dataclass, field
 from fractions import Fraction
@@ -1467,6 +1468,15 @@ class Session:
         self.bounce.clear()
         self.check_errors()
 
+    def power_w(self):
+        """NVML power draw per local device (watts)."""
+        out = {}
+        for d in self.devices:
+            mw = ctypes.c_uint()
+            N.call("cq_nvml_power_mw", d, ctypes.byref(mw))
+            out[d] = mw.value / 1000.0
+        return out
+
     def energy_mj(self):
         out = {}
         for d in self.devices:
@@ -1831,28 +1841,37 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
             the caller gets them); "local" -- each rank fills only what it
             holds; "none" -- results stay on the devices (benchmarking).
     out:    optional {buffer: ndarray} destinations (e.g. ``pinned_empty``).
-    energy: measure NVML energy per device over the run (``measured``).
+    energy: measure NVML energy per device over the run (``measured``; the
+            per-task / per-device report is ``measure.measured_energy``).
     """
     if link is not None and not isinstance(link, LinkModel):
         raise ValidationError("link must be a LinkModel")
     if gather not in ("root", "local", "none"):
         raise ValidationError(f"unknown gather mode '{gather}'")
-    session = Session(plan, placement, trace)
+    session = Session(plan, placement, trace or energy)
     try:
-        e_before = None
+        e_before = idle_w = None
         if energy:
             try:
+                idle_w = session.power_w()      # the devices before the run: the idle baseline
                 e_before = session.energy_mj()
             except NativeError:
                 e_before = None
+        t_before = time.perf_counter()
         session.execute(upload=True)
         session.synchronize()
-        buffers = session.results(gather, out)
+        window = time.perf_counter() - t_before
         measured = {}
         if e_before is not None:
             e_after = session.energy_mj()
+            devs = {}
             for d in session.devices:
-                measured[f"energy_j_device{d}"] = (e_after[d] - e_before[d]) / 1000.0
+                j = (e_after[d] - e_before[d]) / 1000.0
+                measured[f"energy_j_device{d}"] = j
+                devs[d] = {"energy_j": j, "idle_w": idle_w[d], "window_s": window}
+            measured["nvml"] = {"devices": devs,
+                                "node_device": {n: session.dev(n) for n in session.local_nodes}}
+        buffers = session.results(gather, out)
         events, makespan = session.trace()
     finally:
         session.close()

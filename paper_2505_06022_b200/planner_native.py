@@ -15,7 +15,8 @@ from fractions import Fraction
 import numpy as np
 
 from . import _native as N
-from .energy import resolve_target, select_frequency
+from .energy import resolve_target
+from .synergy import select_for_task
 from .model import AccessMode, All, Fixed, Neighborhood, OneToOne, Slice
 from .region import Region, _raw as _mk, _blank as _new, _put as _set
 from .scheduler import (AwaitPushCommand, Chunk, ExecuteCommand, Plan, PushCommand,
@@ -135,11 +136,10 @@ def generate_commands_native(graph, node_count, devices=None, queue_target=None)
             dev = devices[node]
             target = resolve_target(queue_target, task.target)
             vol = box.volume()
-            key = (id(dev), target, vol, task.beta)
+            key = (id(dev), target, vol, task.beta, task.name)
             f = freq_memo.get(key)
             if f is None:
-                f = freq_memo[key] = select_frequency(dev, target, Fraction(vol) / Fraction(dev.throughput_ref),
-                                                      task.beta)
+                f = freq_memo[key] = select_for_task(dev, target, Fraction(vol) / Fraction(dev.throughput_ref), task)
             commands.append(ExecuteCommand(id=cid, deps=deps, chunk=Chunk(task.id, box, node),
                                            frequency_ghz=f, reads=tuple(reads), writes=tuple(writes)))
         elif kind == 1:

@@ -4,9 +4,10 @@ Same schema and key order as the reference CLI (pkg/src/clusterq/cli.py:85-151,
 docs/formats.md:130-186), filled from the executor's measured trace (CUDA
 event times) instead of logical time.  The model energy is the reference's
 ``account_energy`` over those durations; when the run measured NVML energy
-(``run(..., energy=True)``) a ``measured`` section carries the joules per
-device -- kernel_energy_consumption / device_energy_consumption of the paper's
-SYnergy API as real readings.
+(``run(..., energy=True)``) a ``measured`` section carries the NVML joules
+per device and per task (``measure.measured_energy``) --
+kernel_energy_consumption / device_energy_consumption of the paper's SYnergy
+API as real readings.
 """
 
 import json
@@ -37,7 +38,15 @@ def build_report(result, devices=None) -> dict:
         "transfers": {"count": len(pushes), "total_bytes": sum(ev.bytes for ev in pushes)},
     }
     if result.measured:
-        out["measured"] = dict(result.measured)
+        out["measured"] = {k: v for k, v in result.measured.items() if k != "nvml"}
+        if "nvml" in result.measured:
+            from .measure import measured_energy
+            m = measured_energy(result)
+            out["measured"]["per_task"] = [{"id": t.task_id, "name": t.name, "energy_j": float(t.energy_j)}
+                                           for t in m.per_task]
+            out["measured"]["per_device"] = [{"node": d.node, "energy_j": float(d.energy_j),
+                                              "busy_s": float(d.busy_s), "idle_s": float(d.idle_s),
+                                              "idle_w": d.static_power_w} for d in m.per_device]
     return out
 
 

@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 from fractions import Fraction
 
 from . import _native as N
-from .energy import EnergyTarget
+from .energy import DeviceModel, EnergyTarget
 from .errors import NativeError, ValidationError
 
 
@@ -156,3 +156,60 @@ def fit_beta(kernel: MeasuredKernel) -> Fraction:
         num += x * y
         den += x * x
     return num / den
+
+
+class MeasuredDevice(DeviceModel):
+    """A device model backed by measured tables: ``generate_commands`` picks
+    a task's clock with ``select_measured`` over its kernel's (seconds,
+    joules) points instead of the modelled P(f) and t(f) (reference
+    scheduler.py:322-324 calls select_frequency there).  ``kernels`` maps a
+    task name (or "*" for every other task) to its ``MeasuredKernel``; tasks
+    without a table fall back to the model rule over the measured clocks.
+    The levels are the measured clocks in GHz; P(f) for ``account_energy``
+    is the mean measured power (J/s) at that clock over the tables."""
+
+    def __init__(self, kernels: dict, p_static_w: float = 0.0, throughput_ref: float = 1e9, node=None):
+        clocks = sorted({m for k in kernels.values() for m in k.points})
+        if not clocks:
+            raise ValidationError("a measured device needs at least one measured clock")
+        levels = tuple(Fraction(m, 1000) for m in clocks)
+        super().__init__(levels_ghz=tuple(float(x) for x in levels), f_ref_ghz=float(levels[-1]),
+                         p_static_w=p_static_w, p_dyn_ref_w=0.0, alpha_exp=3.0,
+                         throughput_ref=throughput_ref, node=node)
+        object.__setattr__(self, "kernels", dict(kernels))
+
+    def __hash__(self):
+        return id(self)
+
+    def __eq__(self, other):
+        return self is other
+
+    def table_for(self, task_name: str):
+        return self.kernels.get(task_name, self.kernels.get("*"))
+
+    def select_for(self, task_name: str, target: EnergyTarget):
+        """GHz for a task under ``target``, or None without a table."""
+        table = self.table_for(task_name)
+        if table is None:
+            return None
+        return select_measured(table, target) / 1000.0
+
+    def _power_exact(self, f_ghz: float) -> Fraction:
+        mhz = round(float(f_ghz) * 1000)
+        watts = [Fraction(k.points[mhz][1]) / Fraction(k.points[mhz][0])
+                 for k in self.kernels.values() if mhz in k.points]
+        if not watts:
+            raise ValidationError(f"no measured power at {f_ghz} GHz")
+        return sum(watts, Fraction(0)) / len(watts)
+
+
+def select_for_task(device, target: EnergyTarget, t_ref, task) -> float:
+    """The planner's per-chunk clock: a ``MeasuredDevice`` with a table for
+    the task selects over the measurements, any other device uses the
+    reference rule (energy.py:93-106) unchanged."""
+    from .energy import select_frequency
+    if isinstance(device, MeasuredDevice):
+        f = device.select_for(task.name, target)
+        if f is not None:
+            return f
+    return select_frequency(device, target, t_ref, task.beta)

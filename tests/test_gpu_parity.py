@@ -514,3 +514,23 @@ def test_wave_baseline_size_bit_exact():
         res = s.results()
         s.close()
         assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up), nodes
+
+
+def test_kernel_energy_consumption_from_nvml():
+    """SYnergy hooks as readings: run(energy=True) reads
+    the NVML energy counter around the run; kernel_energy_consumption of each
+    task is its duration share of the device's joules above the idle
+    baseline, device_energy_consumption the counter delta."""
+    from paper_2505_06022_b200 import measure
+    n = 262144
+    pos, vel = W.nbody_inputs(n)
+    prog = W.nbody_program(n, steps=6, pos=pos, vel=vel)
+    res = run(cq.generate_commands(prog.graph(), 1), energy=True)
+    dev_j = measure.device_energy_consumption(res)
+    assert dev_j > 0 and res.measured["nvml"]["devices"][0]["idle_w"] > 0
+    kicks = [t for t in prog.graph().tasks if t.name.startswith("kick")]
+    per = [measure.kernel_energy_consumption(res, t.id) for t in kicks]
+    assert all(j > 0 for j in per)
+    rep = measure.measured_energy(res)
+    assert float(rep.total_kernel_energy) <= dev_j + 1e-9
+    assert abs(float(sum(d.energy_j for d in rep.per_device)) - dev_j) < 1e-6

@@ -145,3 +145,50 @@ def test_bench_reference_arm_contract_line():
     for key in ("metric", "unit", "higher_is_better", "config", "scaling", "dtype", "n_gpus", "steps", "warmup"):
         assert mine[key] == d[key], key
     assert d["ms_per_step"] > 0 and "100 time steps per bench step" in d["config"]["workload"]
+
+
+def test_measured_energy_apportions_nvml_joules():
+    """measure.measured_energy: device joules = the NVML delta; idle joules =
+    idle power x the window no execute covers; kernel joules split over the
+    device's executes by duration (SYnergy kernel_energy_consumption /
+    device_energy_consumption as readings)."""
+    from fractions import Fraction as F
+    from paper_2505_06022_b200 import measure
+    from paper_2505_06022_b200.executor import RunResult, TraceEvent
+    tr = [TraceEvent("execute", 0, 0, F(0), F(1, 10), frequency_ghz=2.0, task_id=0, task_name="a"),
+          TraceEvent("execute", 1, 1, F(1, 20), F(1, 10), frequency_ghz=2.0, task_id=0, task_name="a"),
+          TraceEvent("execute", 0, 2, F(2, 10), F(3, 10), frequency_ghz=2.0, task_id=1, task_name="b"),
+          TraceEvent("push", 0, 3, F(1, 10), F(1, 100), bytes=8)]
+    nv = {"devices": {0: {"energy_j": 120.0, "idle_w": 100.0, "window_s": 0.6}},
+          "node_device": {0: 0, 1: 0}}
+    res = RunResult(buffers={}, trace=tr, makespan=F(1, 2), plan=None, measured={"nvml": nv})
+    rep = measure.measured_energy(res)
+    # busy = union [0, 0.15) + [0.2, 0.5) = 0.45 s -> idle 0.15 s x 100 W = 15 J, kernels 105 J
+    assert float(rep.total_kernel_energy) == pytest.approx(105)
+    assert measure.kernel_energy_consumption(res, 1) == pytest.approx(105 * 0.3 / 0.5)
+    assert measure.kernel_energy_consumption(res, 0) == pytest.approx(105 * 0.2 / 0.5)
+    assert float(sum(d.energy_j for d in rep.per_device)) == pytest.approx(120)
+    assert measure.device_energy_consumption(res) == 120.0
+    with pytest.raises(cq.ValidationError):
+        measure.measured_energy(RunResult({}, tr, F(1), None, {}))
+
+
+def test_measured_device_drives_plan_frequencies():
+    """A MeasuredDevice makes generate_commands pick each task's clock with
+    select_measured over its kernel's table (both planners), and
+    account_energy charges the measured power at that clock."""
+    from fractions import Fraction as F
+    from paper_2505_06022_b200 import synergy as S, workloads as W
+    from paper_2505_06022_b200.planner_native import generate_commands_native
+    from paper_2505_06022_b200.scheduler import generate_commands_py
+    saxpy = S.MeasuredKernel("saxpy", {1965: (1.0, 10.0), 1500: (1.1, 8.0), 990: (1.5, 9.0)})
+    other = S.MeasuredKernel("*", {1965: (1.0, 5.0), 1500: (1.3, 6.0), 990: (2.0, 7.0)})
+    dev = S.MeasuredDevice({"saxpy": saxpy, "*": other})
+    assert dev.levels_ghz == (0.99, 1.5, 1.965)
+    prog = W.saxpy_program(4096, kind="float64")
+    for target, want in ((cq.EnergyTarget.MIN_ENERGY, 1.5), (cq.EnergyTarget.MAX_PERF, 1.965),
+                         (cq.EnergyTarget.MIN_EDP, 1.5), (cq.EnergyTarget.MIN_ED2P, 1.5)):
+        for gen in (generate_commands_py, generate_commands_native):
+            plan = gen(prog.graph(), 3, devices=dev, queue_target=target)
+            assert {c.frequency_ghz for c in plan.executes()} == {want}, (target, gen)
+    assert dev.power_watts(1.5) == pytest.approx(float((F(8) / F(11, 10) + F(6) / F(13, 10)) / 2))
