@@ -382,11 +382,16 @@ def bench_wave(args, dist, placement, peaks):
 
     roofline = wave_roofline(dom_kind, dom_launch[1], len(dominant), cells_launch, kern_s, steps_per_launch,
                              bpc, clk, peaks, dist, placement.devices[0], Wd, timing_source)
+    # the PCIe copies bound e2e: the floor for this rank's bytes per simulation
+    link = pcie_floor(placement.devices[0])
+    link["floor_ms_per_step"] = (h2d + d2h) / world / (link["duplex_gbs"] * 1e9) * 1e3
+    link["note"] = ("e2e moves every simulation's inputs in and both fields out over PCIe; floor = "
+                    "(h2d + d2h bytes per rank) / measured duplex rate")
 
     return {
         "value": value, "ms_per_step": dev_ms / args.steps, "plan_s": plan_s,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite,
+                "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite, "pcie": link,
                 "api": f"executor.run_batch (depth {depth}: upload, kernels and read-back of simulations overlap)",
                 "sync": {"value": 12 * cells / sync_s / 1e9, "ms_per_step": sync_s * 1e3 / args.steps,
                          "api": "executor.run (one simulation at a time)"}},
@@ -398,6 +403,43 @@ def bench_wave(args, dist, placement, peaks):
         "execution": execution,
         "H": H, "W": Wd,
     }
+
+
+def pcie_floor(device, nbytes=1 << 30):
+    """The e2e leg's own roofline: concurrent H2D and D2H of ``nbytes`` each
+    between page-locked host memory and the GPU (what one simulation's
+    upload and read-back need), best of 3, through libcq's copy streams."""
+    import ctypes
+    from paper_2505_06022_b200 import _native as N, executor as E
+    src = E.pinned_empty((nbytes // 4,), np.float32)
+    dst = E.pinned_empty((nbytes // 4,), np.float32)
+    src[:] = 1.0
+    d1, d2 = ctypes.c_void_p(), ctypes.c_void_p()
+    N.call("cq_malloc", device, nbytes, ctypes.byref(d1))
+    N.call("cq_malloc", device, nbytes, ctypes.byref(d2))
+    lanes = (N.STREAM_LANE0, N.STREAM_LANE0 + 1)
+
+    def sync():
+        for st in lanes:
+            N.call("cq_stream_synchronize", device, st)
+    best = {}
+    try:
+        for name in ("h2d", "d2h", "duplex"):
+            for _ in range(3):
+                sync()
+                t0 = time.perf_counter()
+                if name in ("h2d", "duplex"):
+                    N.call("cq_copy_h2d", device, lanes[0], d1, ctypes.c_void_p(src.ctypes.data), nbytes)
+                if name in ("d2h", "duplex"):
+                    N.call("cq_copy_d2h", device, lanes[1], ctypes.c_void_p(dst.ctypes.data), d2, nbytes)
+                sync()
+                dt = time.perf_counter() - t0
+                best[name] = min(best.get(name, 1e9), dt)
+    finally:
+        N.call("cq_free", device, d1)
+        N.call("cq_free", device, d2)
+    return {"bytes_each_way": nbytes, "h2d_gbs": nbytes / best["h2d"] / 1e9, "d2h_gbs": nbytes / best["d2h"] / 1e9,
+            "duplex_gbs": 2 * nbytes / best["duplex"] / 1e9}
 
 
 def wave_roofline(kind, cells_per_launch, launches, cells_timed, kern_s, levels, bpc, clk, peaks, dist, device,
@@ -795,6 +837,21 @@ def cpu_kernel_baselines(args, seconds=4.0):
     return out
 
 
+def cpu_baselines_in_subprocess(args, kernels=True):
+    """The CPU legs in a fresh process: this one has torch (and its OpenMP
+    runtime, sized by torchrun's OMP_NUM_THREADS=1 or torch's own setting)
+    loaded, which would pin the C port to fewer threads than the host has."""
+    env = dict(os.environ, OMP_NUM_THREADS=str(os.cpu_count()))
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-only", "--size", str(args.size),
+           "--nbody", str(args.nbody), "--sgemm", str(args.sgemm)] + ([] if kernels else ["--no-kernels"])
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        return json.loads(lines[-1]) if lines else {"wave": {"error": r.stderr[-300:]}}
+    except (OSError, subprocess.TimeoutExpired, ValueError) as exc:
+        return {"wave": {"error": str(exc)[:300]}}
+
+
 def reference_arm(args, dist):
     """--impl reference: the reference's CPU implementation of the path on the
     host cores.  The reference is pure Python (clusterq, ~50 us per cell) and
@@ -910,8 +967,15 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-energy", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="replay via per-command stream dispatch")
+    ap.add_argument("--cpu-only", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.cpu_only:   # the CPU legs of the b200 arm (cpu_baselines_in_subprocess)
+        out = {"wave": cpu_wave_baseline(size=args.size)}
+        if not args.no_kernels:
+            out.update(cpu_kernel_baselines(args))
+        print(json.dumps(out))
+        return 0
     args.sgemm_variants = [v for v in args.sgemm_variants.split(",") if v]
     args.energy = not args.no_energy
 
@@ -936,13 +1000,12 @@ def main():
     kernels = None if args.no_kernels else bench_kernels(args, dist, placement, peaks)
     cpu = None
     if dist.world == 1 and dist.rank == 0 and not args.no_cpu:
-        cpu = cpu_wave_baseline()
-        if kernels is not None:
-            base = cpu_kernel_baselines(args)
-            for key, entry in kernels.items():
-                for name, b in base.items():
-                    if key.startswith(name) and isinstance(entry, dict):
-                        entry["cpu_baseline"] = b
+        base = cpu_baselines_in_subprocess(args, kernels is not None)
+        cpu = base.pop("wave", None)
+        for key, entry in (kernels or {}).items():
+            for name, b in base.items():
+                if key.startswith(name) and isinstance(entry, dict):
+                    entry["cpu_baseline"] = b
     if dist.rank == 0:
         sweep = clock_sweep(args, dist, placement) if args.energy else None
         line = headline_line(args, dist.world, wave, cpu, kernels, sweep)

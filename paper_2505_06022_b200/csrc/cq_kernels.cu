@@ -720,24 +720,24 @@ struct FusedShape {
 };
 
 // Work split.  The pass's work is the output rows [out_lo, out_hi) of every
-// column strip, laid out strip-major (strip 0's rows, then strip 1's, ...)
-// and cut into ranges of `per_warp` rows; range q is the one-warp block q.
-// One-warp blocks keep every per-range quantity (rows, phases, store
+// column strip, cut into pieces of `per_warp` rows; by default (map 2)
+// piece q is strip q % strips, row range q / strips, and it is the
+// one-warp block q -- so consecutive blocks, resident together, march
+// neighbouring strips over the same rows and the strips' shared halo
+// columns come out of L2 once (ncu: 2.31 GB DRAM reads per 16384^2 pass;
+// strip-major ranges read 2.73 GB and ran 26% slower, profiles/r02).
+// One-warp blocks keep every per-piece quantity (rows, phases, store
 // windows) block-uniform, so ptxas proves the warp converged at each
-// shuffle (with a warp index from threadIdx the hot loop carried two
-// divergence checks per row); the block scheduler spreads consecutive
-// ranges -- and with them the slower column-border strips and row-border
-// pieces -- over the SMs.  A range that crosses a strip end is two pieces.  Each
-// piece marches its rows plus 2*KL halo rows in three phases of whole ring
-// turns: full border checks where a level meets row 0 / H-1 or a prefetch
-// leaves [in_lo, in_hi) (first / last turns of border pieces), column
-// checks only for strips touching column 0 / W-1, and the unchecked body
-// (FMA form when the previous pass bounded |X|, else the exact form).
-// One balanced range per warp slot (launch_fused) replaces the earlier 2-D
-// grid of 224-row segments: no half-empty last wave and no partial last
-// block column of 3 busy warps out of 12, and 2*KL halo rows per ~1365
-// rows instead of per 224 (16384^2: 13 x 74 blocks = 6.5 waves -> 147
-// blocks, one per SM).
+// shuffle: with a warp index from threadIdx the hot loop carried two
+// divergence checks and reconvergence barriers per row, the 12-warp block
+// also spilled, and the pass ran 15% slower (profiles/r02/fused_layout_ab.log;
+// CQ_FUSED_WPB / CQ_FUSED_MAP select those layouts for A/B runs).  A range
+// of the strip-major maps (0, 1) that crosses a strip end is two pieces.
+// Each piece marches its rows plus 2*KL halo rows in three phases of whole
+// ring turns: full border checks where a level meets row 0 / H-1 or a
+// prefetch leaves [in_lo, in_hi) (first / last turns of border pieces),
+// column checks only for strips touching column 0 / W-1, and the unchecked
+// body (FMA form when the previous pass bounded |X|, else the exact form).
 // march modes (bit flags): row-border checks, column-border checks, FMA form
 enum { kRows = 1, kCols = 2, kFast = 4, kEdgeAll = kRows | kCols };
 
@@ -915,13 +915,12 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
 // columns / rows and dead lanes included) -- the denominator of the pass's
 // recompute share (bench.py's roofline).
 //
-// Rows per warp range: one block per SM slot and, when the strips divide
-// the warp slots well (>= 95% busy), k = slots / strips ranges per strip of
-// ceil(rows / k) rows (no range crosses a strip end: 16384^2 at KL = 8 is 147
-// strips x 12 ranges of 1366 rows for 1776 warp slots); otherwise an equal
-// share of the strip-major row space.  The 4-step pass is HBM-bound and kept
-// the short ranges it measured fastest with (32 rows, as the earlier 2-D
-// grid's segments).  CQ_FUSED_ROWS=<rows> forces the range length.
+// Rows per piece: 224 for the KL = 8 pass and 24 for the HBM-bound KL = 4
+// pass (interleaved sweeps, profiles/r02/fused_rows_sweep.log: longer
+// pieces cut the halo recompute but every one-wave layout -- 1366 rows,
+// all pieces in flight at once -- ran 10-25% slower), fewer when a launch
+// would not fill the warp slots (short slabs, halo-row edge launches).
+// CQ_FUSED_ROWS=<rows> forces the length.
 struct FusedGeometry {
   int64_t per_warp, blocks, warps, computed_cells;
   int smem, threads, map;
@@ -957,7 +956,7 @@ static int fused_geometry(int64_t rows, int64_t W, FusedGeometry* g) {
   } else {
     // short pieces (profiles/r02 sweeps), shorter still when a launch would
     // not fill the warp slots
-    const int64_t cap = KL == 8 ? 224 : 32, floor_rows = KL == 8 ? 16 : 8;
+    const int64_t cap = KL == 8 ? 224 : 24, floor_rows = KL == 8 ? 16 : 8;
     per = std::min(cap, std::max(floor_rows, (total + slots - 1) / slots));
   }
   per = std::max<int64_t>(1, per);
@@ -1030,11 +1029,9 @@ static int fused_dispatch(int kind, int levels, const FusedLaunch& L) {
     // columns per warp strip
     return levels == 4 ? fused_run<double, 4, 2, 6>(L) : fused_run<double, 8, 2, 6>(L);
   }
-  static int cfg_env = [] {
-    int v = 0, d = 0;
-    if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d", &v, &d);
-    return v ? v * 100 + d : 0;
-  }();
+  int v = 0, d = 0;   // read per launch (A/B sweeps switch it between launches)
+  if (const char* e = getenv("CQ_WAVE_FUSED_CFG")) sscanf(e, "%d,%d", &v, &d);
+  const int cfg_env = v ? v * 100 + d : 0;
   const int cfg = cfg_env ? cfg_env : 4 * 100 + 6;
   switch (cfg * 10 + levels) {
 #define CQ_FUSED_CASE(VV, DD, KL) \

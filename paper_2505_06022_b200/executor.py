@@ -139,6 +139,8 @@ class Placement:
 
 
 _dist_state = {"placement": None, "nccl": False}
+# counts of collective lowerings this process issued (tests / evidence)
+STATS = {"allgather": 0, "nccl_groups": 0}
 
 
 def local_placement() -> Placement:
@@ -771,6 +773,7 @@ class Session:
         def go():
             N.call("cq_nccl_allgather", dev, N.STREAM_COMM, ctypes.c_void_p(v.addr((me * rows,) + ext.mins[1:])),
                    ctypes.c_void_p(v.ptr), rows * row_bytes)
+            STATS["allgather"] += 1
         t = self.issue(dev, N.STREAM_COMM, acc, go)
         for p in pushes:
             if self.local(p.src) or self.local(p.dst):
@@ -811,6 +814,7 @@ class Session:
                             staged.append((v, tmp, box, eb))
                             ptr = tmp
                         plan_ops.append(("recv", ptr, vol * eb, self.rank(p.src)))
+            STATS["nccl_groups"] += 1
             N.call("cq_nccl_group_start")
             for op, ptr, nbytes, peer in plan_ops:
                 fn = "cq_nccl_send" if op == "send" else "cq_nccl_recv"

@@ -90,7 +90,11 @@ def main():
     nb = 4096
     pos, vel = W.nbody_inputs(nb)
     prog = W.nbody_program(nb, steps=2, pos=pos, vel=vel)
+    before = E.STATS["allgather"]
     res = E.run(cq.generate_commands(prog.graph(), world), placement=pl)
+    # the second step's 'all' exchange is one in-place ncclAllGather
+    check(f"nbody {nb} x2 steps: the 'all' exchange ran as ncclAllGather "
+          f"({E.STATS['allgather'] - before} call)", E.STATS["allgather"] - before == 1)
     if rank == 0:
         # the j order is fixed independently of the GPU count, so the
         # distributed result equals a 1-GPU run of the same program bit for bit

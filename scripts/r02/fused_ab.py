@@ -62,8 +62,11 @@ ok = True
 g = torch.Generator(device="cuda").manual_seed(11)
 cases = [(16384, 16384, 0.25), (1000, 1024, 0.25), (517, 384, 0.3), (300, 4096, 0.25), (64, 128, 0.3),
          (2048, 2048, 0.3), (1100, 2176, 0.3), (40, 16384, 0.25), (16384, 256, 0.25)]
-CFGS = [("1", "2", ""), ("1", "2", "7"), ("1", "2", "100"), ("1", "0", "3000"), ("1", "2", "224")]
-for wpb, mp, env in ([] if os.environ.get("SKIP_PARITY") else CFGS):
+CFGS = [("1", "2", ""), ("1", "2", "7"), ("1", "2", "100"), ("1", "0", "3000")]
+CFG_LIST = os.environ.get("PARITY_CFGS", "4,6").split(";")
+for wpb, mp, env, cfg in ([] if os.environ.get("SKIP_PARITY") else
+                          [c + (k,) for k in CFG_LIST for c in CFGS]):
+    os.environ["CQ_WAVE_FUSED_CFG"] = cfg
     os.environ["CQ_FUSED_WPB"] = wpb
     os.environ["CQ_FUSED_MAP"] = mp
     if env:
@@ -77,7 +80,7 @@ for wpb, mp, env in ([] if os.environ.get("SKIP_PARITY") else CFGS):
         b = torch.rand((h, w), device="cuda", generator=g)
         if cc != 0.25:
             a[:, :7] *= 1e-37
-        for kl in (4, 8):
+        for kl in ((8,) if cfg != "4,6" else (4, 8)):
             last, prev = plain(a, b, h, w, kl, cc)
             for fast in (False, True):
                 fl, fp = fused(a, b, h, w, kl, cc, fast)
@@ -97,8 +100,9 @@ for wpb, mp, env in ([] if os.environ.get("SKIP_PARITY") else CFGS):
                 ok &= r
                 if not r:
                     print(f"MISMATCH slab rows={env or 'auto'} {h}x{w} KL={kl}", flush=True)
-    print(f"wpb={wpb} map={mp} rows={env or 'auto'}: parity {'ok' if ok else 'FAILED'}", flush=True)
-os.environ.pop("CQ_FUSED_ROWS", None)
+    print(f"cfg={cfg} wpb={wpb} map={mp} rows={env or 'auto'}: parity {'ok' if ok else 'FAILED'}", flush=True)
+for k in ("CQ_FUSED_ROWS", "CQ_WAVE_FUSED_CFG", "CQ_FUSED_WPB", "CQ_FUSED_MAP"):
+    os.environ.pop(k, None)
 
 
 class Ev:
@@ -170,11 +174,11 @@ def clocks():
         return "?"
 
 
-RUNS8 = [(8, ()), (8, (("CQ_FUSED_ROWS", "160"),)), (8, (("CQ_FUSED_ROWS", "192"),)),
-         (8, (("CQ_FUSED_ROWS", "256"),)), (8, (("CQ_FUSED_ROWS", "342"),)),
-         (8, (("CQ_FUSED_ROWS", "1366"),)), (8, (("CQ_FUSED_MAP", "0"), ("CQ_FUSED_ROWS", "224")))]
-RUNS4 = [(4, ()), (4, (("CQ_FUSED_ROWS", "16"),)), (4, (("CQ_FUSED_ROWS", "24"),)),
-         (4, (("CQ_FUSED_ROWS", "64"),)), (4, (("CQ_FUSED_ROWS", "96"),))]
+RUNS8 = [(8, ()), (8, (("CQ_WAVE_FUSED_CFG", "8,59"),)), (8, (("CQ_WAVE_FUSED_CFG", "8,56"),)),
+         (8, (("CQ_WAVE_FUSED_CFG", "8,62"),)), (8, (("CQ_WAVE_FUSED_CFG", "4,59"),)),
+         (8, (("CQ_WAVE_FUSED_CFG", "8,59"), ("CQ_FUSED_ROWS", "160"))),
+         (8, (("CQ_WAVE_FUSED_CFG", "8,59"), ("CQ_FUSED_ROWS", "320")))]
+RUNS4 = [(4, ()), (4, (("CQ_FUSED_ROWS", "24"),))]
 print("clocks before:", clocks(), flush=True)
 sweep(RUNS8)
 print("clocks:", clocks(), flush=True)
