@@ -80,7 +80,7 @@ for wpb, mp, env, cfg in ([] if os.environ.get("SKIP_PARITY") else
         b = torch.rand((h, w), device="cuda", generator=g)
         if cc != 0.25:
             a[:, :7] *= 1e-37
-        for kl in ((8,) if cfg != "4,6" else (4, 8)):
+        for kl in ((4, 8) if cfg in ("4,6", "4,56") else (8,)):
             last, prev = plain(a, b, h, w, kl, cc)
             for fast in (False, True):
                 fl, fp = fused(a, b, h, w, kl, cc, fast)
@@ -174,11 +174,8 @@ def clocks():
         return "?"
 
 
-RUNS8 = [(8, ()), (8, (("CQ_WAVE_FUSED_CFG", "8,59"),)), (8, (("CQ_WAVE_FUSED_CFG", "8,56"),)),
-         (8, (("CQ_WAVE_FUSED_CFG", "8,62"),)), (8, (("CQ_WAVE_FUSED_CFG", "4,59"),)),
-         (8, (("CQ_WAVE_FUSED_CFG", "8,59"), ("CQ_FUSED_ROWS", "160"))),
-         (8, (("CQ_WAVE_FUSED_CFG", "8,59"), ("CQ_FUSED_ROWS", "320")))]
-RUNS4 = [(4, ()), (4, (("CQ_FUSED_ROWS", "24"),))]
+RUNS8 = [(8, ()), (8, (("CQ_WAVE_FUSED_CFG", "4,56"),))]
+RUNS4 = [(4, ()), (4, (("CQ_WAVE_FUSED_CFG", "4,56"),))]
 print("clocks before:", clocks(), flush=True)
 sweep(RUNS8)
 print("clocks:", clocks(), flush=True)
