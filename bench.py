@@ -495,7 +495,7 @@ def wave_roofline(kind, cells_per_launch, launches, cells_timed, kern_s, levels,
         N.call("cq_wave5_fused_geometry", device, N.CQ_F32, levels, cells_per_launch // width, width, geo)
         computed = geo[3]
         recompute = 1.0 - cells_per_launch / computed
-        geometry = {"rows_per_block": geo[0], "grid": [geo[1], geo[2]], "computed_cells_per_level": computed}
+        geometry = {"rows_per_piece": geo[0], "blocks": geo[1], "warps": geo[2], "computed_cells_per_level": computed}
     except Exception as exc:  # noqa: BLE001
         recompute, geometry = None, {"error": str(exc)[:200]}
     launch_s = kern_s * cells_per_launch / cells_timed   # average launch duration

@@ -186,9 +186,9 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
                            const float* amax_in, float* amax_out);
 
 /* Geometry of one fused pass over `rows` output rows of a W-column grid:
- * out = {rows per block, grid x, grid y, cells computed per level by the
- * launched warps (halo columns / rows included)}.  Host-side query for the
- * roofline's recompute share (bench.py); launches nothing. */
+ * out = {rows per warp piece, blocks, warps, cells computed per level by
+ * the launched warps (halo columns / rows included)}.  Host-side query for
+ * the roofline's recompute share (bench.py); launches nothing. */
 int cq_wave5_fused_geometry(int device, int kind, int levels, int64_t rows, int64_t W, int64_t out[4]);
 
 /* Device interpreter for arbitrary task bodies (eval_kernel, kernel.py:291-331

@@ -174,7 +174,7 @@ def clocks():
         return "?"
 
 
-RUNS8 = [(8, ()), (8, (("CQ_WAVE_FUSED_CFG", "4,56"),))]
+RUNS8 = [(8, ()), (8, (("CQ_WAVE_FUSED_CFG", "4,56"),)), (8, (("CQ_WAVE_FUSED_CFG", "4,59"),))]
 RUNS4 = [(4, ()), (4, (("CQ_WAVE_FUSED_CFG", "4,56"),))]
 print("clocks before:", clocks(), flush=True)
 sweep(RUNS8)
