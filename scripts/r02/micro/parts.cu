@@ -43,11 +43,12 @@ __device__ __forceinline__ void cp16(void* smem, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(g) : "memory");
 }
 
-template <int VAR>
+template <int VAR, int SMODE = 0>
 __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, float4* __restrict__ dst, int iters,
                                                 float c, float* amax_out) {
   constexpr int D = (VAR & 8) ? 6 : 3;
   __shared__ float4 ring[D][2][32];
+  __shared__ __align__(128) float4 stage[2][2][32];   // SMODE 4: rows staged for a TMA bulk store
   const int lane = threadIdx.x;
   float4 L[8][3];
   float4 P[3];
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, 
 #pragma unroll
   for (int k = 0; k < D; ++k) { ring[k][0][lane] = L[0][k % 3]; ring[k][1][lane] = P[k % 3]; }
   const float4* s = src + (blockIdx.x % 64) * 4096 + lane;   // 64 x 64 KB: L2-resident source rows
-  float4* o = dst + (blockIdx.x % 64) * 4096 + lane;
+  float4* o = dst + (size_t)blockIdx.x * 1024 + lane;   // each warp its own 16 rows x 2 x 512 B
   float amax = 0.f;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -88,9 +89,26 @@ __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, 
         const float4 r = cell(mid, L[j - 1][so], L[j - 1][sl], pp, wv, ev, c);
         if (j < 8) L[j][sl] = r;
         if ((VAR & 4) && j >= 7) {
-          const int row = (it * D + sd) & 63;
-          __stcs(o + row * 32 + (j == 8 ? 2048 : 0), r);
-          amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
+          const int row = (it * D + sd) & 15;
+          float4* a = o + row * 32 + (j == 8 ? 512 : 0);
+          if (SMODE == 0 || SMODE == 2) __stcs(a, r);
+          if (SMODE == 1 || SMODE == 3) *a = r;
+          if (SMODE == 4) {
+            // stage the lane's 16 B, then one lane bulk-stores the 512-B row
+            const int buf = sd & 1, k = j == 8;
+            if (k == 0) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+            stage[buf][k][lane] = r;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(&stage[buf][k][0]));
+              asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(a - lane), "r"(sa)
+                           : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+          }
+          if (SMODE == 0 || SMODE == 1 || SMODE == 4)
+            amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
         }
       }
     }
@@ -101,15 +119,15 @@ __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, 
   amax_out[blockIdx.x * 32 + lane] = acc;
 }
 
-template <int VAR>
+template <int VAR, int SMODE = 0>
 void run(const float4* s, float4* d, float* a, int sms, int wps, int iters) {
   const int blocks = sms * wps;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  bench<VAR><<<blocks, 32>>>(s, d, 4, 0.25f, a);
+  bench<VAR, SMODE><<<blocks, 32>>>(s, d, 4, 0.25f, a);
   cudaEventRecord(e0);
-  bench<VAR><<<blocks, 32>>>(s, d, iters, 0.25f, a);
+  bench<VAR, SMODE><<<blocks, 32>>>(s, d, iters, 0.25f, a);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -118,8 +136,9 @@ void run(const float4* s, float4* d, float* a, int sms, int wps, int iters) {
   const double lvl = (double)blocks * iters * D * 8;
   int mhz = 0;
   cudaDeviceGetAttribute(&mhz, cudaDevAttrClockRate, 0);
-  printf("variant %2d (lds %d cp.async %d stores %d unroll %d) warps/SM %2d: %.3f ms, %.1f cycles per level-row per SMSP\n",
-         VAR, VAR & 1, (VAR >> 1) & 1, (VAR >> 2) & 1, D, wps, ms, ms * 1e-3 * (mhz * 1e3) * (sms * 4) / lvl);
+  printf("variant %2d store mode %d (lds %d cp.async %d stores %d unroll %d) warps/SM %2d: %.3f ms, %.1f cycles per "
+         "level-row per SMSP\n", VAR, SMODE, VAR & 1, (VAR >> 1) & 1, (VAR >> 2) & 1, D, wps, ms,
+         ms * 1e-3 * (mhz * 1e3) * (sms * 4) / lvl);
 }
 
 int main() {
@@ -128,17 +147,16 @@ int main() {
   float4 *s, *d;
   float* a;
   cudaMalloc(&s, 64 << 20);
-  cudaMalloc(&d, 64 << 20);
+  cudaMalloc(&d, (size_t)sms * 64 * 1024 * 16);
   cudaMalloc(&a, sms * 64 * 32 * sizeof(float));
   const int iters = 400;
   for (int rep = 0; rep < 2; ++rep) {
-    run<0>(s, d, a, sms, 12, iters * 2);
-    run<1>(s, d, a, sms, 12, iters * 2);
     run<3>(s, d, a, sms, 12, iters * 2);
-    run<5>(s, d, a, sms, 12, iters * 2);
-    run<7>(s, d, a, sms, 12, iters * 2);
-    run<8>(s, d, a, sms, 12, iters);
-    run<15>(s, d, a, sms, 12, iters);
+    run<7, 0>(s, d, a, sms, 12, iters * 2);
+    run<7, 1>(s, d, a, sms, 12, iters * 2);
+    run<7, 2>(s, d, a, sms, 12, iters * 2);
+    run<7, 3>(s, d, a, sms, 12, iters * 2);
+    run<7, 4>(s, d, a, sms, 12, iters * 2);
   }
   return 0;
 }
