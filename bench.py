@@ -471,8 +471,9 @@ def wave_roofline(kind, cells_per_launch, launches, cells_timed, kern_s, levels,
             traffic = t["dram_bytes"] / t["cells"] * cells_per_launch
     effective = dist.min(12 * levels * cells_timed / kern_s / 1e9)
     own = dist.min(bpc * cells_timed / kern_s / 1e9)
-    names = {"wave5_fused8": "wave5_fused_kernel<float,8,4,6,256> (8 time steps per pass)",
-             "wave5_fused4": "wave5_fused_kernel<float,4,4,6,128> (4 time steps per pass)"}
+    names = {"wave5_fused8": "wave5_fused_kernel<float,8,4,6,1> (8 time steps per pass; one-warp blocks, "
+                             "224-row strip-minor pieces)",
+             "wave5_fused4": "wave5_fused_kernel<float,4,4,6,1> (4 time steps per pass; 24-row pieces)"}
     out = {"kernel": names.get(kind, "wave5_rows_kernel<float,32>"), "cells_per_launch": cells_per_launch,
            "launches": launches, "time_steps_per_launch": levels, "launch_timing": timing_source,
            "effective_gbs": effective, "effective_note": "12 B x cells x time steps per launch / launch time "
