@@ -140,7 +140,7 @@ class Placement:
 
 _dist_state = {"placement": None, "nccl": False}
 # counts of collective lowerings this process issued (tests / evidence)
-STATS = {"allgather": 0, "nccl_groups": 0}
+STATS = {"allgather": 0, "nccl_groups": 0, "h2d_bytes": 0, "upload_dedup_bytes": 0}
 
 
 def local_placement() -> Placement:
@@ -672,6 +672,7 @@ class Session:
                         continue
                     N.call("cq_copy_box_h2d", dev, stream, b.itemsize, ctypes.byref(view.c),
                            ctypes.c_void_p(arr.ctypes.data), ctypes.byref(ext), ctypes.byref(cb))
+                    STATS["h2d_bytes"] += box.volume() * b.itemsize
                 else:
                     mode = {"iota": 1, "constant": 2}.get(init.kind, 0)
                     val = float(init.value) if init.kind == "constant" else 0.0
@@ -685,11 +686,44 @@ class Session:
         over node 0's allocation (only what node 0 itself touches)."""
         if not self.local(0):
             return
+        # buffers initialised from the same host array (e.g. a wave's u0 and
+        # up0 = u0) cross PCIe once: the others copy it device to device
+        # (before any kernel, so the first copy still holds version 1)
+        first = {}
         for (node, buf), view in self.views.items():
             if node != 0 or not self.buffers[buf].init.is_initialized:
                 continue
             box = self.seed_box.get((node, buf)) or view.box
-            self.materialize(0, buf, Region.from_box(box), self.h2d_stream)
+            region = Region.from_box(box)
+            key = self._upload_key(buf, box)
+            src = first.get(key) if key is not None else None
+            if src is not None and self.views[(0, src)].device == view.device:
+                self.device_copy(0, src, buf, region, self.h2d_stream)
+                continue
+            self.materialize(0, buf, region, self.h2d_stream)
+            if key is not None:
+                first[key] = buf
+
+    def _upload_key(self, buf, box):
+        """Identity of the host bytes an array-initialised buffer uploads
+        over ``box`` (None for other inits)."""
+        b = self.buffers[buf]
+        if b.init.kind != "array":
+            return None
+        arr = self.host_array(buf)
+        return (arr.__array_interface__["data"][0], arr.dtype.str, arr.shape, arr.strides, box.mins, box.maxs)
+
+    def device_copy(self, node, src_buf, dst_buf, region, stream):
+        """``region`` of node's ``src_buf`` allocation into its ``dst_buf`` one."""
+        src, dst = self.views[(node, src_buf)], self.views[(node, dst_buf)]
+        eb = self.buffers[dst_buf].itemsize
+
+        def go():
+            for box in region.boxes:
+                N.call("cq_copy_box", dst.device, stream, eb, ctypes.byref(dst.c), dst.device, ctypes.byref(src.c),
+                       src.device, ctypes.byref(_cbox(box)))
+                STATS["upload_dedup_bytes"] += box.volume() * eb
+        return self.issue(dst.device, stream, [(node, src_buf, region, False), (node, dst_buf, region, True)], go)
 
     # ---- transfers -------------------------------------------------------
     def flush_group(self, group):
@@ -697,12 +731,23 @@ class Session:
         if not group:
             return
         nccl_ops = []
+        first = {}   # host bytes -> buffer already materialised at that node in this group
         for push in group:
             src_l, dst_l = self.local(push.src), self.local(push.dst)
             if not push.deps:
-                # host-initialised data: the destination materialises it
+                # host-initialised data: the destination materialises it; the
+                # same host bytes for a second buffer are a device copy
                 if dst_l and self.uploading:
-                    t = self.materialize(push.dst, push.buffer, push.region, self.h2d_stream)
+                    box = push.region.bounding_box()
+                    key = self._upload_key(push.buffer, box)
+                    key = None if key is None or len(push.region.boxes) != 1 else (push.dst,) + key
+                    src = first.get(key) if key is not None else None
+                    if src is not None:
+                        t = self.device_copy(push.dst, src, push.buffer, push.region, self.h2d_stream)
+                    else:
+                        t = self.materialize(push.dst, push.buffer, push.region, self.h2d_stream)
+                        if key is not None:
+                            first[key] = push.buffer
                     self.mark_transfer(push, push.dst, t)
                 continue
             if src_l and dst_l:
