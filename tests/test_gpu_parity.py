@@ -128,8 +128,8 @@ def test_wave_bit_exact_vs_oracle(nodes, kind):
 @pytest.mark.parametrize("nodes,steps,c", [(1, 22, 0.25), (1, 100, 0.25), (3, 22, 0.3), (4, 36, 0.3),
                                            (2, 9, 0.25), (1, 26, 0.1)])
 def test_fused_wave_chain_bit_exact_vs_oracle(nodes, steps, c):
-    """Temporal blocking (cq_wave5_fused: KL=4 blocks, one KL=8 parity
-    block, KL-row halo exchange between slabs, plain leftovers) reproduces
+    """Temporal blocking (cq_wave5_fused: a KL=4 quarter block, then KL=8
+    blocks, KL-row halo exchange between slabs, plain leftovers) reproduces
     the per-step oracle bit for bit -- also for a c whose products round
     (c = 0.3, 0.1) and subnormal neighbourhoods, where an FMA contraction of
     c*lap + (2u - upr) would differ."""
@@ -148,6 +148,31 @@ def test_fused_wave_chain_bit_exact_vs_oracle(nodes, steps, c):
     s.close()
     assert any(k.startswith("wave5_fused") for k in kinds)
     u, up = onat.wave_run(u0, up0, steps, c)
+    assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
+
+
+@pytest.mark.parametrize("layout", [{"CQ_FUSED_ROWS": "7"}, {"CQ_FUSED_ROWS": "100"},
+                                    {"CQ_FUSED_ROWS": "3000", "CQ_FUSED_MAP": "0"},
+                                    {"CQ_FUSED_MAP": "1", "CQ_FUSED_WPB": "12"},
+                                    {"CQ_FUSED_ROWS": "64", "CQ_FUSED_MAP": "2", "CQ_FUSED_WPB": "12"}])
+def test_fused_wave_piece_layouts_bit_exact(layout, monkeypatch):
+    """Every piece layout of the fused pass (rows per warp piece that split
+    strips unevenly or cross strip ends, strip-major or strip-minor maps,
+    12-warp blocks) gives the per-step oracle's bits, FMA-form blocks and
+    slab edges included."""
+    from paper_2505_06022_b200.executor import Placement, Session
+    for k, v in layout.items():
+        monkeypatch.setenv(k, v)
+    h, w = 700, 1792
+    u0 = np.random.default_rng(23).uniform(0, 1, (h, w)).astype(np.float32)
+    prog = W.wave_program(h, w, steps=20, kind="float32", c=0.3, u0=u0, up0=u0)
+    s = Session(cq.generate_commands(prog.graph(), 3), Placement(1, 0, (0,)))
+    assert [b.kl for b in s.chains[0].blocks] == [4, 8, 8]
+    s.execute(upload=True)
+    s.synchronize()
+    res = s.results()
+    s.close()
+    u, up = onat.wave_run(u0, u0, 20, 0.3)
     assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up)
 
 
