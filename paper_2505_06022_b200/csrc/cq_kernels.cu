@@ -686,6 +686,14 @@ __device__ __forceinline__ Vec wave_vec_fast(Vec m, Vec n, Vec s, Vec p, decltyp
 __device__ __forceinline__ float abs_max(float4 v) { return fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))); }
 __device__ __forceinline__ float abs_max(float2 v) { return fmaxf(fabsf(v.x), fabsf(v.y)); }
 __device__ __forceinline__ float abs_max(double2 v) { return (float)fmax(fabs(v.x), fabs(v.y)); }
+// running max |x| of stored vectors: two 3-input FMNMX per float4
+__device__ __forceinline__ float amax_with(float m, float4 v) {
+  m = fmaxf(fmaxf(m, fabsf(v.x)), fabsf(v.y));
+  return fmaxf(fmaxf(m, fabsf(v.z)), fabsf(v.w));
+}
+__device__ __forceinline__ float amax_with(float m, float2 v) { return fmaxf(fmaxf(m, fabsf(v.x)), fabsf(v.y)); }
+__device__ __forceinline__ float amax_with(float m, double2 v) { return fmaxf(m, abs_max(v)); }
+
 
 __device__ __forceinline__ void cp_async_row(void* smem, const void* gmem, bool valid, int bytes) {
   const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -832,9 +840,13 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
       if (q < nrow) fetch(std::integral_constant<int, kEdgeAll>{}, q, q, ub + (int64_t)q * us, pb + (int64_t)q * ps);
       cp_async_commit();
     }
-    // one input row: land it, prefetch row t + D, advance every level
-    auto row = [&](auto mode, const int t, const int sd) {
+    // one input row: land it, prefetch row t + D, advance levels 1..LM.
+    // (Skipping level j before iteration 2j, its first row of the
+    // trapezoid, in a prologue saved 3.75% of the level-rows but cost the
+    // main loop 29 register moves per turn: not kept.)
+    auto row = [&](auto mode, auto lm, const int t, const int sd) {
       constexpr int M = decltype(mode)::value;
+      constexpr int LM = decltype(lm)::value;
       const int s = sd % 3, so = (sd + 1) % 3, sm = (sd + 2) % 3;  // rows t, t-2, t-1
       cp_async_wait<D - 1>();  // row t (the oldest group) has landed
       L[0][s] = ring[(sd * 2 + 0) * 32 + lane];
@@ -844,7 +856,7 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
       uf += us;
       pf += ps;
 #pragma unroll
-      for (int j = 1; j <= KL; ++j) {
+      for (int j = 1; j <= LM; ++j) {
         const Vec mid = L[j - 1][sm];
         Vec nn = L[j - 1][so], ss = L[j - 1][s];
         T wv = __shfl_up_sync(0xffffffffu, last_of(mid), 1);
@@ -864,14 +876,14 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
         if (j == KL - 1 && t >= prev_lo && t < prev_hi) {
           if (keep) {
             __stcs(reinterpret_cast<Vec*>(sp), o);
-            amax = fmaxf(amax, abs_max(o));
+            amax = amax_with(amax, o);
           }
           sp += pstr;
         }
         if (j == KL && t >= last_lo) {
           if (keep) {
             __stcs(reinterpret_cast<Vec*>(sl), o);
-            amax = fmaxf(amax, abs_max(o));
+            amax = amax_with(amax, o);
           }
           sl += ls;
         }
@@ -879,11 +891,12 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
     };
     // whole ring turns without a bounds test (the warp stays converged, so
     // the shuffles need no collective fallback), then the remainder
+    using AllLevels = std::integral_constant<int, KL>;
     auto turns = [&](auto mode, int& t, const int end) {
 #pragma unroll 1
       for (; t < end; t += D) {
 #pragma unroll
-        for (int sd = 0; sd < D; ++sd) row(mode, t + sd, sd);
+        for (int sd = 0; sd < D; ++sd) row(mode, AllLevels{}, t + sd, sd);
       }
     };
     int t = 0;
@@ -898,7 +911,7 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
     turns(std::integral_constant<int, kEdgeAll>{}, t, nfull);
 #pragma unroll
     for (int sd = 0; sd < D; ++sd)
-      if (nfull + sd < nrow) row(std::integral_constant<int, kEdgeAll>{}, nfull + sd, sd);
+      if (nfull + sd < nrow) row(std::integral_constant<int, kEdgeAll>{}, AllLevels{}, nfull + sd, sd);
     cp_async_wait<0>();
   }
   if (amax_out != nullptr) {
