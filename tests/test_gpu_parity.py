@@ -559,3 +559,34 @@ def test_kernel_energy_consumption_from_nvml():
     rep = measure.measured_energy(res)
     assert float(rep.total_kernel_energy) <= dev_j + 1e-9
     assert abs(float(sum(d.energy_j for d in rep.per_device)) - dev_j) < 1e-6
+
+
+def test_measured_device_from_nvml_plans_and_runs():
+    """The measured-table policy on hardware: a wave task's (seconds, joules)
+    per iteration measured with NVML at the running SM clock
+    (synergy.kernel_energy; clocks are never changed on this pool) feeds a
+    MeasuredDevice; both planners then label every execute with that clock,
+    and the run's measured energy report covers every task."""
+    from paper_2505_06022_b200 import measure, synergy as S
+    from paper_2505_06022_b200.executor import Placement, Session
+    from paper_2505_06022_b200.planner_native import generate_commands_native
+    from paper_2505_06022_b200.scheduler import generate_commands_py
+    n, steps = 4096, 16
+    u0 = W.wave_pulse(n, n, "float32")
+    prog = W.wave_program(n, n, steps=steps, kind="float32", c=0.25, u0=u0, up0=u0)
+    s = Session(cq.generate_commands(prog.graph(), 1), Placement(1, 0, (0,)), trace=False)
+    s.execute(upload=True)
+    s.synchronize()
+    s.recycle()
+    s.capture()
+    r = S.kernel_energy(lambda: s.replay(1), 0, seconds=0.5, sync=s.synchronize)
+    s.close()
+    assert r["j_per_call"] > 0 and r["sm_mhz"] > 0
+    table = S.MeasuredKernel("*", {r["sm_mhz"]: (r["s_per_call"] / steps, r["j_per_call"] / steps)})
+    dev = S.MeasuredDevice({"*": table})
+    for gen in (generate_commands_py, generate_commands_native):
+        plan = gen(prog.graph(), 1, devices=dev, queue_target=cq.EnergyTarget.MIN_EDP)
+        assert {c.frequency_ghz for c in plan.executes()} == {r["sm_mhz"] / 1000.0}
+    res = run(plan, energy=True)
+    rep = measure.measured_energy(res)
+    assert len(rep.per_task) == steps and float(rep.total_device_energy) > 0
