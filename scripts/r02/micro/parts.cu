@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, 
   constexpr int D = (VAR & 8) ? 6 : 3;
   __shared__ float4 ring[D][2][32];
   __shared__ __align__(128) float4 stage[2][2][32];   // SMODE 4: rows staged for a TMA bulk store
+  __shared__ __align__(128) float4 stage5[2][D][2][32];  // SMODE 5: a turn of rows, double-buffered
   const int lane = threadIdx.x;
   float4 L[8][3];
   float4 P[3];
@@ -107,10 +108,32 @@ __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, 
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
           }
-          if (SMODE == 0 || SMODE == 1 || SMODE == 4)
+          if (SMODE == 5) stage5[it & 1][sd][j == 8][lane] = r;
+          if (SMODE == 0 || SMODE == 1 || SMODE == 4 || SMODE == 5)
             amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
         }
       }
+    }
+    if ((VAR & 4) && SMODE == 5) {
+      // the turn's 2 x D rows leave in bulk copies issued by one lane; the
+      // other half of the staging buffer must have been read out before it
+      // is rewritten next turn
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+#pragma unroll
+        for (int sd = 0; sd < D; ++sd)
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const int row = (it * D + sd) & 15;
+            const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(&stage5[it & 1][sd][k][0]));
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(o - lane + row * 32 + k * 512),
+                         "r"(sa) : "memory");
+          }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      __syncwarp();
     }
   }
   float acc = amax;
@@ -157,6 +180,13 @@ int main() {
     run<7, 2>(s, d, a, sms, 12, iters * 2);
     run<7, 3>(s, d, a, sms, 12, iters * 2);
     run<7, 4>(s, d, a, sms, 12, iters * 2);
+    run<7, 5>(s, d, a, sms, 12, iters * 2);
+    run<15, 0>(s, d, a, sms, 12, iters);
+    run<15, 5>(s, d, a, sms, 12, iters);
+    run<8>(s, d, a, sms, 12, iters);
+    run<9>(s, d, a, sms, 12, iters);
+    run<11>(s, d, a, sms, 12, iters);
+    run<13>(s, d, a, sms, 12, iters);
   }
   return 0;
 }
