@@ -94,6 +94,12 @@ __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, 
           float4* a = o + row * 32 + (j == 8 ? 512 : 0);
           if (SMODE == 0 || SMODE == 2) __stcs(a, r);
           if (SMODE == 1 || SMODE == 3) *a = r;
+          if (SMODE == 6 && j == 8) __stcs(a, r);                       // one store per row
+          if (SMODE == 7) stage[sd & 1][j == 8][lane] = r;              // shared-memory stores only
+          if (SMODE == 8) {                                              // two 8-byte stores
+            __stcs(reinterpret_cast<float2*>(a), make_float2(r.x, r.y));
+            __stcs(reinterpret_cast<float2*>(a) + 1, make_float2(r.z, r.w));
+          }
           if (SMODE == 4) {
             // stage the lane's 16 B, then one lane bulk-stores the 512-B row
             const int buf = sd & 1, k = j == 8;
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(32, 12) bench(const float4* __restrict__ src, 
             }
           }
           if (SMODE == 5) stage5[it & 1][sd][j == 8][lane] = r;
-          if (SMODE == 0 || SMODE == 1 || SMODE == 4 || SMODE == 5)
+          if (SMODE == 0 || SMODE == 1 || SMODE == 4 || SMODE == 5 || SMODE >= 6)
             amax = fmaxf(amax, fmaxf(fmaxf(fabsf(r.x), fabsf(r.y)), fmaxf(fabsf(r.z), fabsf(r.w))));
         }
       }
@@ -174,6 +180,11 @@ int main() {
   cudaMalloc(&a, sms * 64 * 32 * sizeof(float));
   const int iters = 400;
   for (int rep = 0; rep < 2; ++rep) {
+    run<13, 0>(s, d, a, sms, 12, iters);
+    run<13, 6>(s, d, a, sms, 12, iters);
+    run<13, 7>(s, d, a, sms, 12, iters);
+    run<13, 8>(s, d, a, sms, 12, iters);
+    run<9, 0>(s, d, a, sms, 12, iters);
     run<3>(s, d, a, sms, 12, iters * 2);
     run<7, 0>(s, d, a, sms, 12, iters * 2);
     run<7, 1>(s, d, a, sms, 12, iters * 2);
