@@ -1881,6 +1881,25 @@ def _default_sgemm():
     return os.environ.get("CQ_SGEMM", "3xtf32")
 
 
+def _nvml_step(session, timeout_s: float = 1.0):
+    """{device: (perf_counter time, mJ)} at the next step of each device's
+    NVML energy counter.  The counter advances in coarse steps (tens of ms),
+    so a run shorter than a step read between two plain reads can see no
+    change at all; a window that starts and ends on a step holds exactly the
+    joules of that window (its idle tail is charged at idle power by
+    ``measure.measured_energy``)."""
+    start = session.energy_mj()
+    t0 = time.perf_counter()
+    out = {}
+    while len(out) < len(start):
+        now_mj = session.energy_mj()
+        t = time.perf_counter()
+        for d, v in now_mj.items():
+            if d not in out and (v != start[d] or t - t0 > timeout_s):
+                out[d] = (t, v)
+    return out
+
+
 def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
         out: Optional[dict] = None, trace: bool = True, energy: bool = False,
         placement: Optional[Placement] = None) -> RunResult:
@@ -1903,21 +1922,19 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
         if energy:
             try:
                 idle_w = session.power_w()      # the devices before the run: the idle baseline
-                e_before = session.energy_mj()
+                e_before = _nvml_step(session)
             except NativeError:
                 e_before = None
-        t_before = time.perf_counter()
         session.execute(upload=True)
         session.synchronize()
-        window = time.perf_counter() - t_before
         measured = {}
         if e_before is not None:
-            e_after = session.energy_mj()
+            e_after = _nvml_step(session)
             devs = {}
             for d in session.devices:
-                j = (e_after[d] - e_before[d]) / 1000.0
+                j = (e_after[d][1] - e_before[d][1]) / 1000.0
                 measured[f"energy_j_device{d}"] = j
-                devs[d] = {"energy_j": j, "idle_w": idle_w[d], "window_s": window}
+                devs[d] = {"energy_j": j, "idle_w": idle_w[d], "window_s": e_after[d][0] - e_before[d][0]}
             measured["nvml"] = {"devices": devs,
                                 "node_device": {n: session.dev(n) for n in session.local_nodes}}
         buffers = session.results(gather, out)

@@ -1,12 +1,14 @@
 """Measured SYnergy energy: NVML joules behind the reference's energy hooks.
 
 The reference charges model watts to logical time (energy.py:150-197).  A
-B200 run with ``run(plan, energy=True)`` reads, per device, the NVML energy
-counter and the idle power just before the run and the counter again after
-it (``RunResult.measured["nvml"]``); ``measured_energy`` turns that into the
-reference's ``EnergyReport``:
+B200 run with ``run(plan, energy=True)`` reads, per device, the idle power
+before the run and the NVML energy counter at the counter step just before
+the run and at the first step after it (``RunResult.measured["nvml"]``;
+the counter advances in steps of tens of ms, so a window between two plain
+reads can miss a short run entirely); ``measured_energy`` turns that into
+the reference's ``EnergyReport``:
 
-* device joules = the counter delta over the run window;
+* device joules = the counter delta over the window between the two steps;
 * idle joules = the pre-run idle power x the window time no execute covers
   (union of the device's execute intervals, CUDA-event times);
 * kernel joules = device joules - idle joules, split over the device's

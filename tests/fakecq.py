@@ -479,14 +479,16 @@ class FakeNvmlLib(FakeLib):
 
     CLOCKS = (1965, 1800, 1500, 1200, 990, 600)
 
-    def __init__(self, *a, allow_lock=True, **kw):
+    def __init__(self, *a, allow_lock=True, tick_s=0.0, **kw):
         super().__init__(*a, **kw)
         import time as _t
         self._t = _t
         self.mhz = max(self.CLOCKS)
         self.allow_lock = allow_lock
+        self.tick_s = tick_s  # > 0: the counter publishes in steps, like NVML's
         self._mj = 0.0
-        self._last = _t.perf_counter()
+        self._last = self._tick = _t.perf_counter()
+        self._published = 0
 
     def _power_w(self):
         return 200.0 + 800.0 * (self.mhz / max(self.CLOCKS)) ** 3
@@ -501,7 +503,9 @@ class FakeNvmlLib(FakeLib):
 
     def cq_nvml_energy_mj(self, d, p):
         self._advance()
-        _obj(p).value = int(self._mj)
+        if self.tick_s <= 0 or self._last - self._tick >= self.tick_s:
+            self._published, self._tick = int(self._mj), self._last
+        _obj(p).value = self._published
         return 0
 
     def cq_nvml_power_mw(self, d, p):
