@@ -568,3 +568,60 @@ def test_shared_host_input_crosses_pcie_once(fake):
         assert up_bytes == (1 if same else 2) * h * w * 4 and dedup == (h * w * 4 if same else 0)
         u, up = onat.wave_run(u0, up0, 3, 0.25)
         assert dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up)
+
+
+# ------------------------------------------------------- 8 ranks over gloo
+
+def _rank8_main(rank, world, port, outdir):
+    """The bench's shapes at 8 ranks (the driver's largest scaling point):
+    a fused wave chain over 8 row slabs (KL-row exchanges between every
+    neighbour pair, weak-scaled rows like bench.py) and the N-body 'all'
+    mapper as one all-gather across the 8 ranks."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = FakeLib(1, GlooTransport())
+    N._lib = lib
+    pl = E.Placement(world, rank, (0,))
+    results = {}
+    u0 = np.random.default_rng(12).uniform(0, 1, (40 * world, 16)).astype(np.float32)
+    prog = W.wave_program(40 * world, 16, steps=12, kind="float32", u0=u0, up0=u0)
+    sess = E.Session(cq.generate_commands(prog.graph(), world), pl)
+    assert [b.kl for b in sess.chains[0].blocks] == [4, 8]
+    sess.execute(upload=True)
+    sess.synchronize()
+    res = sess.results()
+    sess.close()
+    if rank == 0:
+        results["u"], results["up"] = res["u"], res["up"]
+    pos, vel = W.nbody_inputs(8 * world)
+    before = len(lib.launches)
+    res = E.run(cq.generate_commands(W.nbody_program(8 * world, steps=2, pos=pos, vel=vel).graph(), world),
+                placement=pl)
+    results[f"allgathers_r{rank}"] = np.array(
+        [sum(1 for x in lib.launches[before:] if isinstance(x, tuple) and x[0] == "allgather")])
+    if rank == 0:
+        results["P"], results["V"] = res.buffers["P"], res.buffers["V"]
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), **results)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_eight_ranks_gloo(tmp_path):
+    import torch.multiprocessing as mp
+    from oracle import native as onat
+    world = 8
+    mp.start_processes(_rank8_main, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    r = [dict(np.load(tmp_path / f"rank{k}.npz")) for k in range(world)]
+    u0 = np.random.default_rng(12).uniform(0, 1, (40 * world, 16)).astype(np.float32)
+    u, up = onat.wave_run(u0, u0, 12, 0.25)
+    assert dsl.same_bits(r[0]["u"], u) and dsl.same_bits(r[0]["up"], up)
+    assert all(int(x[f"allgathers_r{k}"][0]) == 1 for k, x in enumerate(r))
+    pos, vel = W.nbody_inputs(8 * world)
+    N._lib = FakeLib(1, LocalTransport())
+    single = E.run(cq.generate_commands(W.nbody_program(8 * world, steps=2, pos=pos, vel=vel).graph(), 1),
+                   placement=E.Placement(1, 0, (0,)))
+    N._lib = None
+    assert dsl.same_bits(r[0]["P"], single.buffers["P"]) and dsl.same_bits(r[0]["V"], single.buffers["V"])
