@@ -25,23 +25,23 @@ def view(t, h, w):
     return v
 
 
-def fused(vs, h, w, kl, rows=None):
+def fused(vs, h, w, kl, rows=None, fast=True):
     ext = N.box3((0, 0), (h, w))
     lo, hi = rows or (0, h)
-    bound[0] = 1.0
+    bound[0] = 1.0 if fast else float("inf")
     N.call("cq_wave5_fused_bounded", 0, 0, N.CQ_F32, kl, ctypes.byref(vs[0]), ctypes.byref(vs[1]),
            ctypes.byref(vs[2]), ctypes.byref(vs[3]), lo, hi, lo + (kl if rows else 0), hi - (kl if rows else 0),
            ctypes.byref(ext), C, K2, K4, ctypes.c_void_p(bound.data_ptr()), ctypes.c_void_p(bound.data_ptr() + 4))
 
 
-def check(h, w, kl, slab):
+def check(h, w, kl, slab, fast):
     g = torch.Generator(device="cuda").manual_seed(5)
     a, b = torch.rand((h, w), device="cuda", generator=g), torch.rand((h, w), device="cuda", generator=g)
     a[:, :5] *= 1e-37
     ol, op = torch.full_like(a, float("nan")), torch.full_like(a, float("nan"))
     torch.cuda.synchronize()
     rows = (h // 4, 3 * h // 4) if slab else None
-    fused([view(x, h, w) for x in (a, b, ol, op)], h, w, kl, rows)
+    fused([view(x, h, w) for x in (a, b, ol, op)], h, w, kl, rows, fast)
     x, y = a.clone(), b.clone()
     torch.cuda.synchronize()
     ext = N.box3((0, 0), (h, w))
@@ -55,7 +55,15 @@ def check(h, w, kl, slab):
         torch.equal(op[s].view(torch.int32), y[s].view(torch.int32))
 
 
-ok = all(check(h, w, kl, slab) for (h, w) in ((4096, 4096), (517, 384)) for kl in (4, 8) for slab in (False, True))
+SHAPES = ((4096, 4096), (517, 384), (1000, 1000), (40, 1024), (300, 2176), (2048, 16384), (129, 256))
+ok = True
+for (h, w) in SHAPES:
+    for kl in (4, 8):
+        for slab in (False, True):
+            for fast in (False, True):
+                if not check(h, w, kl, slab, fast):
+                    ok = False
+                    print(f"MISMATCH {h}x{w} KL={kl} slab={slab} fast={fast}", flush=True)
 
 
 class Ev:
@@ -92,5 +100,5 @@ for kl in (8, 4, 8):
     res.setdefault(kl, []).append(ts[len(ts) // 2])
 clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader"],
                      capture_output=True, text=True).stdout.strip()
-print(f"{os.path.basename(os.environ.get('CQ_LIB', 'libcq.so'))}: parity {'ok' if ok else 'FAILED'}; "
+print(f"{os.path.basename(os.environ.get('CQ_LIB', 'libcq.so'))} cfg={os.environ.get('CQ_WAVE_FUSED_CFG', 'default')}: parity {'ok' if ok else 'FAILED'}; "
       f"KL=8 median {min(res[8]):.4f} ms, KL=4 {res[4][0]:.4f} ms; clocks after: {clk}", flush=True)
