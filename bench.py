@@ -390,12 +390,15 @@ def bench_wave(args, dist, placement, peaks):
     roofline = wave_roofline(dom_kind, dom_launch[1], len(dominant), cells_launch, kern_s, steps_per_launch,
                              bpc, clk, peaks, dist, placement.devices[0], Wd, timing_source)
     # the PCIe copies bound e2e: the floor for this rank's bytes per simulation
-    link = pcie_floor(placement.devices[0])
-    b_in, b_out = h2d / world, d2h / world
-    link["floor_ms_per_step"] = max(b_in / (link["h2d_gbs"] * 1e9), b_out / (link["d2h_gbs"] * 1e9),
-                                    (b_in + b_out) / (link["duplex_gbs"] * 1e9)) * 1e3
-    link["note"] = ("e2e moves every simulation's inputs in and both fields out over PCIe; floor = the "
-                    "slowest of h2d bytes / h2d rate, d2h bytes / d2h rate and both / the duplex rate, per rank")
+    b_in, b_out = h2d // world, d2h // world
+    link = pcie_floor(placement.devices[0], pattern=(b_in - b_in % 16, b_out - b_out % 16))
+    link["floor_model_ms"] = max(b_in / (link["h2d_gbs"] * 1e9), b_out / (link["d2h_gbs"] * 1e9),
+                                 (b_in + b_out) / (link["duplex_gbs"] * 1e9)) * 1e3
+    link["floor_ms_per_step"] = link["pattern_ms"]
+    link["note"] = ("e2e moves every simulation's inputs in and both fields out over PCIe; floor = one "
+                    "simulation's own H2D and D2H bytes copied concurrently with nothing else running "
+                    "(pattern_ms, per rank); floor_model_ms = the slowest of h2d bytes / h2d rate, d2h bytes "
+                    "/ d2h rate and both / the 1:1 duplex rate")
 
     return {
         "value": value, "ms_per_step": dev_ms / args.steps, "plan_s": plan_s,
@@ -414,41 +417,52 @@ def bench_wave(args, dist, placement, peaks):
     }
 
 
-def pcie_floor(device, nbytes=1 << 30):
-    """The e2e leg's own roofline: concurrent H2D and D2H of ``nbytes`` each
-    between page-locked host memory and the GPU (what one simulation's
-    upload and read-back need), best of 3, through libcq's copy streams."""
+def pcie_floor(device, nbytes=1 << 30, pattern=None):
+    """The e2e leg's own roofline: H2D, D2H and concurrent H2D + D2H of
+    ``nbytes`` each between page-locked host memory and the GPU, and, with
+    ``pattern`` = (h2d bytes, d2h bytes), one simulation's actual transfers
+    issued concurrently with nothing else running (best of 3 each, through
+    libcq's copy streams)."""
     import ctypes
     from paper_2505_06022_b200 import _native as N, executor as E
-    src = E.pinned_empty((nbytes // 4,), np.float32)
-    dst = E.pinned_empty((nbytes // 4,), np.float32)
+    up, down = pattern or (nbytes, nbytes)
+    big = max(nbytes, up, down)
+    src = E.pinned_empty((big // 4,), np.float32)
+    dst = E.pinned_empty((big // 4,), np.float32)
     src[:] = 1.0
     d1, d2 = ctypes.c_void_p(), ctypes.c_void_p()
-    N.call("cq_malloc", device, nbytes, ctypes.byref(d1))
-    N.call("cq_malloc", device, nbytes, ctypes.byref(d2))
+    N.call("cq_malloc", device, big, ctypes.byref(d1))
+    N.call("cq_malloc", device, big, ctypes.byref(d2))
     lanes = (N.STREAM_LANE0, N.STREAM_LANE0 + 1)
 
     def sync():
         for st in lanes:
             N.call("cq_stream_synchronize", device, st)
     best = {}
+    sizes = {"h2d": (nbytes, 0), "d2h": (0, nbytes), "duplex": (nbytes, nbytes)}
+    if pattern:
+        sizes["pattern"] = (up, down)
     try:
-        for name in ("h2d", "d2h", "duplex"):
+        for name, (b_in, b_out) in sizes.items():
             for _ in range(3):
                 sync()
                 t0 = time.perf_counter()
-                if name in ("h2d", "duplex"):
-                    N.call("cq_copy_h2d", device, lanes[0], d1, ctypes.c_void_p(src.ctypes.data), nbytes)
-                if name in ("d2h", "duplex"):
-                    N.call("cq_copy_d2h", device, lanes[1], ctypes.c_void_p(dst.ctypes.data), d2, nbytes)
+                if b_in:
+                    N.call("cq_copy_h2d", device, lanes[0], d1, ctypes.c_void_p(src.ctypes.data), b_in)
+                if b_out:
+                    N.call("cq_copy_d2h", device, lanes[1], ctypes.c_void_p(dst.ctypes.data), d2, b_out)
                 sync()
                 dt = time.perf_counter() - t0
                 best[name] = min(best.get(name, 1e9), dt)
     finally:
         N.call("cq_free", device, d1)
         N.call("cq_free", device, d2)
-    return {"bytes_each_way": nbytes, "h2d_gbs": nbytes / best["h2d"] / 1e9, "d2h_gbs": nbytes / best["d2h"] / 1e9,
-            "duplex_gbs": 2 * nbytes / best["duplex"] / 1e9}
+    out = {"bytes_each_way": nbytes, "h2d_gbs": nbytes / best["h2d"] / 1e9, "d2h_gbs": nbytes / best["d2h"] / 1e9,
+           "duplex_gbs": 2 * nbytes / best["duplex"] / 1e9}
+    if pattern:
+        out["pattern_bytes"] = [up, down]
+        out["pattern_ms"] = best["pattern"] * 1e3
+    return out
 
 
 def wave_roofline(kind, cells_per_launch, launches, cells_timed, kern_s, levels, bpc, clk, peaks, dist, device,
