@@ -426,13 +426,13 @@ def pcie_floor(device, nbytes=1 << 30, pattern=None):
     import ctypes
     from paper_2505_06022_b200 import _native as N, executor as E
     up, down = pattern or (nbytes, nbytes)
-    big = max(nbytes, up, down)
-    src = E.pinned_empty((big // 4,), np.float32)
-    dst = E.pinned_empty((big // 4,), np.float32)
+    n_in, n_out = max(nbytes, up), max(nbytes, down)
+    src = E.pinned_empty((n_in // 4,), np.float32)
+    dst = E.pinned_empty((n_out // 4,), np.float32)
     src[:] = 1.0
     d1, d2 = ctypes.c_void_p(), ctypes.c_void_p()
-    N.call("cq_malloc", device, big, ctypes.byref(d1))
-    N.call("cq_malloc", device, big, ctypes.byref(d2))
+    N.call("cq_malloc", device, n_in, ctypes.byref(d1))
+    N.call("cq_malloc", device, n_out, ctypes.byref(d2))
     lanes = (N.STREAM_LANE0, N.STREAM_LANE0 + 1)
 
     def sync():
