@@ -368,12 +368,17 @@ def bench_wave(args, dist, placement, peaks):
     # following ones the PCIe duplex floor; scripts/r02/e2e_diag*.py)
     E.run_batch(plan, [(None, outs[k % depth]) for k in range(max(2 * depth, args.warmup))], gather=gather,
                 depth=depth)
-    dist.barrier()
-    h2d0 = E.STATS["h2d_bytes"]
-    t0 = time.perf_counter()
-    batch = E.run_batch(plan, [(None, outs[k % depth]) for k in range(args.steps)], gather=gather, depth=depth)
-    e2e_s = dist.max(time.perf_counter() - t0)
-    h2d = int(dist.sum((E.STATS["h2d_bytes"] - h2d0) / args.steps))   # bytes that crossed PCIe per simulation
+    # three timed batches of K simulations each, the median reported (a box
+    # has shown one-off batches at 2-3x its usual time; all three are listed)
+    batches_s = []
+    for _rep in range(3):
+        dist.barrier()
+        h2d0 = E.STATS["h2d_bytes"]
+        t0 = time.perf_counter()
+        batch = E.run_batch(plan, [(None, outs[k % depth]) for k in range(args.steps)], gather=gather, depth=depth)
+        batches_s.append(dist.max(time.perf_counter() - t0))
+        h2d = int(dist.sum((E.STATS["h2d_bytes"] - h2d0) / args.steps))   # bytes that crossed PCIe per simulation
+    e2e_s = sorted(batches_s)[1]
     e2e = 12 * cells / e2e_s / 1e9
     res_buffers = batch[-1]
     E.run(plan, gather=gather, out=outs[0], trace=False)
@@ -404,6 +409,8 @@ def bench_wave(args, dist, placement, peaks):
         "value": value, "ms_per_step": dev_ms / args.steps, "plan_s": plan_s,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3 / args.steps, "gather": gather, "finite": finite, "pcie": link,
+                "batches_ms_per_step": [b * 1e3 / args.steps for b in batches_s],
+                "timing": "median of three timed run_batch calls of --steps simulations each",
                 "api": f"executor.run_batch (depth {depth}: upload, kernels and read-back of simulations overlap)",
                 "sync": {"value": 12 * cells / sync_s / 1e9, "ms_per_step": sync_s * 1e3 / args.steps,
                          "api": "executor.run (one simulation at a time)"}},

@@ -661,20 +661,17 @@ __device__ __forceinline__ float4 wave_vec_fast(float4 m, float4 n, float4 s, fl
   // t = fma(2, u, -p): the same addends as fl(2u) + (-p), so also the same
   // signed zero when 2u == p (the form -fma(-2, u, p) gives -0 there)
   const f32x2 tA = fma2(uA, two, pack2(-p.x, -p.y)), tB = fma2(uB, two, pack2(-p.z, -p.w));
-  // c*lap packed; its unpacked halves feed scalar adds, which ptxas does not
-  // contract (checked in the SASS: no scalar FFMA in this kernel)
-  const f32x2 cc = pack2(c, c);
-  const f32x2 clA = mul2(cc, lapA), clB = mul2(cc, lapB);
-  float l0, l1, l2, l3, t0, t1, t2, t3;
-  unpack2(clA, l0, l1);
-  unpack2(clB, l2, l3);
-  unpack2(tA, t0, t1);
-  unpack2(tB, t2, t3);
+  // c*lap as fma(c, lap, +0), then a packed add: an FFMA2 result is not a
+  // product ptxas can contract into the add.  fl(c*lap + 0) == fl(c*lap)
+  // except for an exact -0 product (+0 instead), i.e. lap == -0 when c > 0,
+  // which needs u == +0; then t = fl(2u - p) is never -0, and t + (-0) ==
+  // t + (+0).  So for c > 0 (the host enables this form only then) the bits
+  // are those of the DSL's t + c*lap.
+  const f32x2 cc = pack2(c, c), zero = pack2(0.f, 0.f);
+  const f32x2 oA = add2(tA, fma2(cc, lapA, zero)), oB = add2(tB, fma2(cc, lapB, zero));
   float4 o;
-  o.x = __fadd_rn(t0, l0);
-  o.y = __fadd_rn(t1, l1);
-  o.z = __fadd_rn(t2, l2);
-  o.w = __fadd_rn(t3, l3);
+  unpack2(oA, o.x, o.y);
+  unpack2(oB, o.z, o.w);
   return o;
 }
 template <typename Vec>
@@ -1196,7 +1193,10 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
     const char* e = getenv("CQ_WAVE_FAST");
     return !(e && e[0] == '0');
   }();
-  const float limit = fast_ok ? (float)(std::ldexp(1.0, 124) / std::pow(3.0 + 8.0 * std::fabs(c) + 1e-3, levels)) : 0.f;
+  // (and c > 0: the form's c*lap + 0 product, see wave_vec_fast)
+  const float limit = fast_ok && c > 0.0
+                          ? (float)(std::ldexp(1.0, 124) / std::pow(3.0 + 8.0 * std::fabs(c) + 1e-3, levels))
+                          : 0.f;
   FusedLaunch L{st, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, amax_in, amax_out,
                 limit, nullptr};
   CQ_TRY(fused_dispatch(kind, levels, L));
