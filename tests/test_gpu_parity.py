@@ -243,11 +243,12 @@ def test_fused_wave_chain_fast_form_bit_exact(scale, c):
         assert dsl.same_bits(res["u"], u) and dsl.same_bits(res["up"], up), (scale, c, nodes)
 
 
-@pytest.mark.parametrize("c", [0.3, -0.2])
+@pytest.mark.parametrize("c", [0.3, -0.2, 0.25, 0.0])
 def test_fused_wave_chain_fast_form_signed_zeros(c):
     """Fields of +0 / -0 and the smallest subnormals: exact cancellations
     (2u == p) and products underflowing to -0 must give the tree's signed
-    zeros in the FMA form too (t = fma(2, u, -p), not -fma(-2, u, p))."""
+    zeros in the FMA form too (t = fma(2, u, -p), not -fma(-2, u, p); c*lap
+    as fma(c, lap, +0), taken only for c > 0; c <= 0 keeps the exact form)."""
     from paper_2505_06022_b200.executor import Placement, Session
     h, w, steps = 768, 3072, 40   # interior CTAs exist (see above)
     rng = np.random.default_rng(33)
