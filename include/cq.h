@@ -143,6 +143,9 @@ int cq_nccl_group_end(void);
 int cq_nccl_send(int device, int stream, const void* buf, int64_t bytes, int peer);
 int cq_nccl_recv(int device, int stream, void* buf, int64_t bytes, int peer);
 int cq_nccl_allgather(int device, int stream, const void* send, void* recv, int64_t bytes_per_rank);
+/* In-place broadcast of `bytes` at `buf` from rank `root` (ncclBroadcast): one
+ * source node's region pushed to every other node (SURVEY §8b cq_bcast). */
+int cq_nccl_bcast(int device, int stream, void* buf, int64_t bytes, int root);
 int cq_nccl_destroy(void);
 
 /* ----------------------------------------------------------------- kernels */

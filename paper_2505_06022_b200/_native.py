@@ -98,6 +98,7 @@ _SIGS = {
     "cq_nccl_send": (i32, [i32, i32, vp, i64, i32]),
     "cq_nccl_recv": (i32, [i32, i32, vp, i64, i32]),
     "cq_nccl_allgather": (i32, [i32, i32, vp, vp, i64]),
+    "cq_nccl_bcast": (i32, [i32, i32, vp, i64, i32]),
     "cq_nccl_destroy": (i32, []),
     "cq_fill": (i32, [i32, i32, i32, P(CqView), P(CqBox), P(CqBox), i32, ctypes.c_double, i64]),
     "cq_saxpy": (i32, [i32, i32, i32, ctypes.c_double, i64, vp, vp, vp, i64]),

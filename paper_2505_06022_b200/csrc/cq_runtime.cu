@@ -624,6 +624,13 @@ int cq_nccl_allgather(int device, int stream, const void* send, void* recv, int6
   return CQ_OK;
 }
 
+int cq_nccl_bcast(int device, int stream, void* buf, int64_t bytes, int root) {
+  CQ_STREAM(device, stream);
+  CQ_REQUIRE(g_comm && device == g_comm_device, "NCCL not initialised for device %d", device);
+  CQ_CHECK_NCCL(ncclBroadcast(buf, buf, (size_t)bytes, ncclChar, root, g_comm, st));
+  return CQ_OK;
+}
+
 int cq_nccl_destroy(void) {
   if (g_comm) {
     ncclCommDestroy(g_comm);

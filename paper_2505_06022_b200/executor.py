@@ -140,7 +140,7 @@ class Placement:
 
 _dist_state = {"placement": None, "nccl": False}
 # counts of collective lowerings this process issued (tests / evidence)
-STATS = {"allgather": 0, "nccl_groups": 0, "h2d_bytes": 0, "upload_dedup_bytes": 0}
+STATS = {"allgather": 0, "bcast": 0, "nccl_groups": 0, "h2d_bytes": 0, "upload_dedup_bytes": 0}
 
 
 def local_placement() -> Placement:
@@ -757,9 +757,13 @@ class Session:
         if nccl_ops:
             # the 'all' exchange is recognised on the whole group (identical
             # on every rank), then this rank's part of it posted
-            layout = self._allgather_layout([p for p in group if p.deps])
+            dev_pushes = [p for p in group if p.deps]
+            layout = self._allgather_layout(dev_pushes)
+            bcast = self._bcast_layout(dev_pushes) if layout is None else None
             if layout is not None:
                 self.allgather(nccl_ops, *layout)
+            elif bcast is not None:
+                self.bcast(nccl_ops, *bcast)
             else:
                 self.nccl_group(nccl_ops)
 
@@ -803,6 +807,47 @@ class Session:
         if v is None or v.box != ext:
             return None
         return buf, S
+
+    def _bcast_layout(self, pushes):
+        """(buffer, box, root) when ``pushes`` send one box of one buffer from
+        one node to every other node (e.g. an 'all' or 'fixed' read of data a
+        single node wrote), node k being rank k and the box a contiguous run
+        of whole rows in every rank's allocation -- then one in-place
+        ncclBroadcast replaces the G-1 sends (SURVEY.md §8b cq_bcast)."""
+        G = self.nodes
+        if self.pl.world < 2 or G != self.pl.world or len(pushes) != G - 1:
+            return None
+        p0 = pushes[0]
+        if len(p0.region.boxes) != 1 or self.rank(p0.src) != p0.src:
+            return None
+        box = p0.region.boxes[0]
+        if any(p.buffer != p0.buffer or p.src != p0.src or p.region.boxes != p0.region.boxes for p in pushes):
+            return None
+        if {p.dst for p in pushes} != set(range(G)) - {p0.src}:
+            return None
+        # whole rows of the buffer: contiguous in every rank's allocation (each
+        # holds the box), and decided from the plan alone, so identically on
+        # every rank
+        ext = self.buffers[p0.buffer].extent
+        if box.mins[1:] != ext.mins[1:] or box.maxs[1:] != ext.maxs[1:]:
+            return None
+        return p0.buffer, box, p0.src
+
+    def bcast(self, pushes, buf, box, root):
+        """One in-place broadcast of ``box`` of ``buf`` from ``root`` on the comm stream."""
+        dev = self.pl.devices[0]
+        me = self.pl.rank
+        v = self.views[(me, buf)]
+        nbytes = box.volume() * self.buffers[buf].itemsize
+        acc = [(me, buf, Region.from_box(box), me != root)]
+
+        def go():
+            N.call("cq_nccl_bcast", dev, N.STREAM_COMM, ctypes.c_void_p(v.addr(box.mins)), nbytes, root)
+            STATS["bcast"] += 1
+        t = self.issue(dev, N.STREAM_COMM, acc, go)
+        for p in pushes:
+            if self.local(p.src) or self.local(p.dst):
+                self.mark_transfer(p, p.src if self.local(p.src) else p.dst, t)
 
     def allgather(self, pushes, buf, rows):
         """One in-place all-gather of ``buf``'s slabs on the comm stream."""

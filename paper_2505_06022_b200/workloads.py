@@ -168,3 +168,22 @@ def sgemm_program(m, n, k, variant="3xtf32", a=None, b=None) -> Program:
                  Accessor("C", W, name="c")],
                 NativeKernel("sgemm", variant))
     return Program("sgemm", bufs, [task])
+
+
+# --------------------------------------------------------- row broadcast
+
+def row_broadcast_program(rows, cols=64, kind="float32") -> Program:
+    """One row ``c`` written by node 0 alone (a one-row task), then read in
+    full by every node's chunk of a ``rows``-row task through an 'all'
+    mapper: node 0 pushes the row to every other node (one ncclBroadcast
+    across ranks).  d[i, j] = (2 a_j + 1) * 3 + i with a = iota."""
+    one, grid = Box.from_shape((1, cols)), Box.from_shape((rows, cols))
+    bufs = {"a": Buffer("a", one, kind, BufferInit.iota()),
+            "c": Buffer("c", one, kind, BufferInit.zeros()),
+            "d": Buffer("d", grid, kind, BufferInit.zeros())}
+    make = Task("make", one, [Accessor("a", R), Accessor("c", W)],
+                {"c": parse_kernel("a[i.0, i.1] * 2 + 1", {"a": 2}, set(), 2)})
+    use = Task("use", grid, [Accessor("c", R, All()), Accessor("d", W)],
+               {"d": parse_kernel("c[i.0, i.1] * 3 + i.0", {"c": 2}, set(), 2)})
+    return Program("row_broadcast", bufs, [make, use])
+

@@ -123,6 +123,15 @@ def main():
             err = np.abs(res.buffers["C"][rows] - c) / cabs
             check(f"sgemm {variant} {m}x{nn}x{k} err={err.max():.2e}", err.max() <= 1e-6)
 
+    # one node's row pushed to every other node: one in-place ncclBroadcast
+    before = E.STATS["bcast"]
+    res = E.run(cq.generate_commands(W.row_broadcast_program(4 * world).graph(), world), placement=pl)
+    if rank == 0:
+        rows, cols = 4 * world, 64
+        want = ((2 * np.arange(cols, dtype=np.float32) + 1) * 3)[None, :] + np.arange(rows, dtype=np.float32)[:, None]
+        check(f"row broadcast nodes={world}: one ncclBroadcast ({E.STATS['bcast'] - before}), values exact",
+              E.STATS["bcast"] - before == (1 if world > 1 else 0) and np.array_equal(res.buffers["d"], want))
+
     dist.barrier()
     E.shutdown_distributed()
     dist.destroy_process_group()

@@ -220,6 +220,12 @@ class FakeLib:
         self.launches.append(("allgather", int(_val(n))))
         return 0
 
+    def cq_nccl_bcast(self, d, s, buf, n, root):
+        """In-place ncclBroadcast semantics over the transport."""
+        self.transport.bcast(self, _val(buf), int(_val(n)), int(_val(root)))
+        self.launches.append(("bcast", int(_val(n))))
+        return 0
+
     def cq_nccl_destroy(self):
         return 0
 
@@ -551,6 +557,9 @@ class LocalTransport:
     def allgather(self, lib, send, recv, n):
         raise AssertionError("NCCL all-gather issued in a single-process run")
 
+    def bcast(self, lib, buf, n, root):
+        raise AssertionError("NCCL broadcast issued in a single-process run")
+
 
 class GlooTransport:
     """NCCL group semantics over torch.distributed (gloo): all sends and
@@ -586,6 +595,13 @@ class GlooTransport:
         dist.all_gather(out, t)
         for r, o in enumerate(out):
             lib._mem(recv + r * n, n)[:] = o.numpy()
+
+    def bcast(self, lib, buf, n, root):
+        import torch
+        import torch.distributed as dist
+        t = torch.from_numpy(lib._mem(buf, n).copy())
+        dist.broadcast(t, root)
+        lib._mem(buf, n)[:] = t.numpy()
 
 
 def _graph_api(cls):

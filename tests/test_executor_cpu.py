@@ -625,3 +625,37 @@ def test_eight_ranks_gloo(tmp_path):
                    placement=E.Placement(1, 0, (0,)))
     N._lib = None
     assert dsl.same_bits(r[0]["P"], single.buffers["P"]) and dsl.same_bits(r[0]["V"], single.buffers["V"])
+
+
+# ------------------------------------------------- broadcast over 3 ranks
+
+def _rank_bcast_main(rank, world, port, outdir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lib = FakeLib(1, GlooTransport())
+    N._lib = lib
+    plan = cq.generate_commands(W.row_broadcast_program(4 * world).graph(), world)
+    res = E.run(plan, placement=E.Placement(world, rank, (0,)))
+    n_b = sum(1 for x in lib.launches if isinstance(x, tuple) and x[0] == "bcast")
+    n_g = sum(1 for x in lib.launches if isinstance(x, tuple) and x[0] == "group")
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), d=res.buffers.get("d", np.zeros(0)), n=np.array([n_b, n_g]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_single_source_push_group_is_one_broadcast(tmp_path):
+    """A push group sending one node's rows of a buffer to every other node
+    is lowered to one in-place ncclBroadcast (cq_nccl_bcast) on every rank,
+    with the same results as one process."""
+    import torch.multiprocessing as mp
+    world = 3
+    mp.start_processes(_rank_bcast_main, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    r = [dict(np.load(tmp_path / f"rank{k}.npz")) for k in range(world)]
+    R, C = 4 * world, 64
+    want = ((2 * np.arange(C, dtype=np.float32) + 1) * 3)[None, :] + np.arange(R, dtype=np.float32)[:, None]
+    assert np.array_equal(r[0]["d"], want)
+    for k in range(world):
+        assert int(r[k]["n"][0]) == 1, r[k]["n"]   # one broadcast, no send/recv group for it
