@@ -21,7 +21,7 @@ outs = [{"u": E.pinned_empty((H, Wd), np.float32, box), "up": E.pinned_empty((H,
         for _ in range(6)]
 E.run_batch(plan, [(None, outs[k % 3]) for k in range(6)], gather="root", depth=3)
 for rep in range(2):
-    for depth in (2, 3, 4, 6):
+    for depth in (1, 2, 3, 4):
         t0 = time.perf_counter()
         E.run_batch(plan, [(None, outs[k % depth]) for k in range(12)], gather="root", depth=depth)
         print(f"depth {depth}: {(time.perf_counter() - t0) / 12 * 1e3:.1f} ms/simulation", flush=True)
