@@ -38,7 +38,8 @@ enum {
   CQ_ERR_PERMISSION = 5,
   CQ_ERR_UNSUPPORTED = 6,
   CQ_ERR_EVAL = 7,     /* integer division by zero  -> EvalError            */
-  CQ_ERR_MAPPER = 8    /* read outside mapped region -> MapperViolationError */
+  CQ_ERR_MAPPER = 8,   /* read outside mapped region -> MapperViolationError */
+  CQ_ERR_P2P = 9       /* a peer's halo signal did not arrive in time (device flag) */
 };
 
 enum { CQ_F64 = 0, CQ_F32 = 1, CQ_I64 = 2 };
@@ -148,6 +149,25 @@ int cq_nccl_allgather(int device, int stream, const void* send, void* recv, int6
 int cq_nccl_bcast(int device, int stream, void* buf, int64_t bytes, int root);
 int cq_nccl_destroy(void);
 
+/* ------------------------------------------ peer memory (CUDA IPC, NVLink)
+ * The temporally blocked wave's halo rows go straight into the neighbouring
+ * rank's allocations (copy-engine writes through IPC-opened pointers) instead
+ * of a per-pass NCCL exchange; device-side counters order the passes. */
+/* IPC handle (64 bytes) of an allocation's base pointer (cq_malloc blocks). */
+int cq_ipc_handle(const void* ptr, unsigned char handle_out[64]);
+/* Open a peer process's allocation on `device`; *ptr is valid for copies and
+ * device stores until cq_ipc_close. */
+int cq_ipc_open(int device, const unsigned char handle[64], void** ptr);
+int cq_ipc_close(int device, void* ptr);
+/* Block `stream` until every non-null `slot_k` (a local word written by a
+ * peer) holds a value >= *count (a local word); after `timeout_ns` the wait
+ * gives up and sets the device error flag (CQ_ERR_P2P) instead of hanging. */
+int cq_p2p_wait(int device, int stream, const uint64_t* slot0, const uint64_t* slot1, const uint64_t* count,
+                int64_t timeout_ns);
+/* *count += 1, then store the new value (release, system scope) to every
+ * non-null peer word. */
+int cq_p2p_signal(int device, int stream, uint64_t* count, uint64_t* peer0, uint64_t* peer1);
+
 /* ----------------------------------------------------------------- kernels */
 /* Host-initialised contents of node 0 (BufferInit.materialize, model.py:63-74):
  * mode 0 zeros, 1 iota (row-major index within `extent`), 2 constant. */
@@ -187,6 +207,41 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
                            const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
                            int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4,
                            const float* amax_in, float* amax_out);
+/* A peer rank's output allocations (CUDA IPC pointers) that also receive
+ * the rows [row_lo, row_hi) a fused pass writes: X(t+KL) rows to `last`, X(t+KL-1)
+ * rows to `prev`; the cell (r, c) lives at base + (r - row0) * stride + (c - col0). */
+typedef struct {
+  void* last;
+  void* prev;
+  int64_t row0, col0, stride;
+  int64_t row_lo, row_hi;
+} cq_mirror_t;
+
+/* In-pass ordering with the neighbouring ranks (executor._PeerHalo): the
+ * blocks whose pieces read halo rows / store mirrored rows first wait until
+ * every non-null local `slot` (written by a neighbour) >= *count, and the last
+ * of them to finish increments *count and stores it (release, system scope)
+ * to every non-null `peer_slot`, after raising every non-null `peer_amax` with
+ * its rows' max |x|.  `done` is a local zeroed counter. */
+typedef struct {
+  const uint64_t* slot[2];
+  uint64_t* count;
+  uint32_t* done;
+  uint64_t* peer_slot[2];
+  float* peer_amax[2];    /* the neighbours' amax_out words: edge blocks raise them too */
+  int64_t timeout_ns;
+} cq_peer_sync_t;
+
+/* cq_wave5_fused_bounded whose FMA form (amax_in) covers only pieces reading
+ * rows inside [fast_lo, fast_hi) -- e.g. not a neighbour's halo rows, which
+ * the local bound does not cover; the others keep the exact form -- and whose
+ * output rows inside a mirror's range are also stored to that peer (up to 2;
+ * the storing blocks end with a system-scope fence). */
+int cq_wave5_fused_ex(int device, int stream, int kind, int levels, const cq_view_t* u, const cq_view_t* upr,
+                      const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
+                      int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4,
+                      const float* amax_in, float* amax_out, int64_t fast_lo, int64_t fast_hi,
+                      const cq_mirror_t* mirrors, int n_mirrors, const cq_peer_sync_t* sync);
 
 /* Geometry of one fused pass over `rows` output rows of a W-column grid:
  * out = {rows per warp piece, blocks, warps, cells computed per level by

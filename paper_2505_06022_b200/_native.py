@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CQ_LIB", os.path.join(HERE, "libcq.so"))
 
 CQ_OK, CQ_ERR_CUDA, CQ_ERR_NCCL, CQ_ERR_NVML, CQ_ERR_ARG = 0, 1, 2, 3, 4
-CQ_ERR_PERMISSION, CQ_ERR_UNSUPPORTED, CQ_ERR_EVAL, CQ_ERR_MAPPER = 5, 6, 7, 8
+CQ_ERR_PERMISSION, CQ_ERR_UNSUPPORTED, CQ_ERR_EVAL, CQ_ERR_MAPPER, CQ_ERR_P2P = 5, 6, 7, 8, 9
 CQ_F64, CQ_F32, CQ_I64 = 0, 1, 2
 STREAM_COMPUTE, STREAM_BOUNDARY, STREAM_COMM = 0, 1, 2
 STREAM_LANE0, NUM_LANES = 3, 8
@@ -39,6 +39,20 @@ class CqBox(ctypes.Structure):
 
 class CqView(ctypes.Structure):
     _fields_ = [("ptr", vp), ("alloc", CqBox), ("stride", i64 * 3)]
+
+
+class CqPeerSync(ctypes.Structure):
+    """cq_peer_sync_t: in-pass ordering with the neighbouring ranks."""
+    _fields_ = [("slot", ctypes.c_void_p * 2), ("count", ctypes.c_void_p), ("done", ctypes.c_void_p),
+                ("peer_slot", ctypes.c_void_p * 2), ("peer_amax", ctypes.c_void_p * 2),
+                ("timeout_ns", ctypes.c_int64)]
+
+
+class CqMirror(ctypes.Structure):
+    """cq_mirror_t: peer allocations that also receive some output rows of a fused pass."""
+    _fields_ = [("last", ctypes.c_void_p), ("prev", ctypes.c_void_p), ("row0", ctypes.c_int64),
+                ("col0", ctypes.c_int64), ("stride", ctypes.c_int64), ("row_lo", ctypes.c_int64),
+                ("row_hi", ctypes.c_int64)]
 
 
 class CqExpr(ctypes.Structure):
@@ -99,6 +113,11 @@ _SIGS = {
     "cq_nccl_recv": (i32, [i32, i32, vp, i64, i32]),
     "cq_nccl_allgather": (i32, [i32, i32, vp, vp, i64]),
     "cq_nccl_bcast": (i32, [i32, i32, vp, i64, i32]),
+    "cq_ipc_handle": (i32, [vp, vp]),
+    "cq_ipc_open": (i32, [i32, vp, P(vp)]),
+    "cq_ipc_close": (i32, [i32, vp]),
+    "cq_p2p_wait": (i32, [i32, i32, vp, vp, vp, i64]),
+    "cq_p2p_signal": (i32, [i32, i32, vp, vp, vp]),
     "cq_nccl_destroy": (i32, []),
     "cq_fill": (i32, [i32, i32, i32, P(CqView), P(CqBox), P(CqBox), i32, ctypes.c_double, i64]),
     "cq_saxpy": (i32, [i32, i32, i32, ctypes.c_double, i64, vp, vp, vp, i64]),
@@ -109,6 +128,9 @@ _SIGS = {
     "cq_wave5_fused_bounded": (i32, [i32, i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqView), i64, i64,
                                      i64, i64, P(CqBox), ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      vp, vp]),
+    "cq_wave5_fused_ex": (i32, [i32, i32, i32, i32, P(CqView), P(CqView), P(CqView), P(CqView), i64, i64,
+                                i64, i64, P(CqBox), ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                vp, vp, i64, i64, vp, i32, vp]),
     "cq_wave5_fused_geometry": (i32, [i32, i32, i32, i64, i64, P(i64)]),
     "cq_expr_eval": (i32, [i32, i32, P(CqExpr)]),
     "cq_error_flag": (i32, [i32, P(i32), P(i64), i32]),

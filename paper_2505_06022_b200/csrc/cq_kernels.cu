@@ -91,6 +91,41 @@ __device__ void report_error(unsigned long long* flag, int code, int64_t lin, in
   }
 }
 
+// ------------------------------------------------------- peer pass ordering
+// One thread spins until every given slot (a local word a neighbour's
+// p2p_signal_kernel writes) reaches *count; gives up after timeout_ns and
+// records CQ_ERR_P2P in the sticky error flag rather than hang the stream.
+__global__ void p2p_wait_kernel(const unsigned long long* slot0, const unsigned long long* slot1,
+                                const unsigned long long* count, long long timeout_ns,
+                                unsigned long long* flag) {
+  const unsigned long long want = *count;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (const unsigned long long* sl : {slot0, slot1}) {
+    if (sl == nullptr) continue;
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sl) : "memory");
+      if (v >= want) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if ((long long)(t - t0) > timeout_ns) {
+        report_error(flag, CQ_ERR_P2P, 0, (int64_t)want, (int64_t)v, 0);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+__global__ void p2p_signal_kernel(unsigned long long* count, unsigned long long* peer0,
+                                  unsigned long long* peer1) {
+  const unsigned long long v = *count + 1;
+  *count = v;
+  __threadfence_system();  // the pass's stores and copies before the signal
+  if (peer0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer0), "l"(v) : "memory");
+  if (peer1) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer1), "l"(v) : "memory");
+}
+
 // ------------------------------------------------------------------- fill
 template <typename T>
 __global__ void fill_kernel(cq_view_t dst, cq_box_t box, cq_box_t extent, int mode, T value) {
@@ -746,13 +781,66 @@ struct FusedShape {
 // march modes (bit flags): row-border checks, column-border checks, FMA form
 enum { kRows = 1, kCols = 2, kFast = 4, kEdgeAll = kRows | kCols };
 
-template <typename T, int KL, int V, int D, int WPB>
+// Up to two peer allocations (CUDA IPC pointers) that also receive some of
+// the pass's output rows: the neighbouring ranks' halo rows for their next
+// pass, written over NVLink while the pass runs (executor._PeerHalo).
+struct FusedMirrors {
+  cq_mirror_t m[2];
+  int n;
+  cq_peer_sync_t sync;
+  int sync_on, n_edge;  // blocks with an edge piece (the last one signals)
+};
+
+// an edge block waits for the neighbours' previous pass (their rows for this
+// one are in place, and they no longer read the rows this one sends them)
+__device__ __forceinline__ void edge_wait(const FusedMirrors& mir, unsigned long long* flag) {
+  const unsigned long long want = *(volatile unsigned long long*)mir.sync.count;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const unsigned long long* sl = (const unsigned long long*)mir.sync.slot[k];
+    if (sl == nullptr) continue;
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sl) : "memory");
+      if (v >= want) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if ((long long)(t - t0) > mir.sync.timeout_ns) {
+        report_error(flag, CQ_ERR_P2P, 0, (int64_t)want, (int64_t)v, 0);
+        return;
+      }
+      __nanosleep(32);
+    }
+  }
+}
+
+// the last edge block of the pass: count += 1, published to the neighbours
+__device__ __forceinline__ void edge_done(const FusedMirrors& mir) {
+  __threadfence_system();
+  if (atomicAdd((unsigned int*)mir.sync.done, 1u) == (unsigned int)mir.n_edge - 1) {
+    *(volatile unsigned int*)mir.sync.done = 0;
+    const unsigned long long v = *(volatile unsigned long long*)mir.sync.count + 1;
+    *(volatile unsigned long long*)mir.sync.count = v;
+    __threadfence_system();
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (mir.sync.peer_slot[k] != nullptr)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(mir.sync.peer_slot[k]), "l"(v) : "memory");
+  }
+}
+
+// PEER: the multi-rank variant (peer stores, in-pass ordering, per-piece
+// bound); without it the kernel compiles exactly as the single-GPU pass.
+template <typename T, int KL, int V, int D, int WPB, bool PEER>
 __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB)
     wave5_fused_kernel(cq_view_t u, cq_view_t upr, cq_view_t out_last, cq_view_t out_prev, int64_t in_lo,
                        int64_t in_hi, int64_t out_lo, int64_t out_hi, int64_t H, int64_t W, T c,
                        int64_t per_warp, int map, const float* __restrict__ amax_in,
-                       float* __restrict__ amax_out, float limit) {
+                       float* __restrict__ amax_out, float limit, int64_t fast_lo, int64_t fast_hi,
+                       const __grid_constant__ FusedMirrors mir, unsigned long long* err_flag) {
   typedef typename FVec<T, V>::T Vec;
+  bool mirrored = false;  // this block stored rows to a peer
   static_assert(KL >= 2 && KL % V == 0, "strip offsets must stay vector aligned");
   static_assert(D % 3 == 0, "prefetch ring must be a multiple of the window");
   constexpr int SW = 32 * V - 2 * KL;
@@ -812,6 +900,21 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
     int t2 = (int)(bot >= nfull ? nfull : bot / D * D);
     if (t2 < t1) t2 = t1;
     const bool col_edge = !(c0 > 0 && c0 + 32 * V < W);
+    // the bound covers rows [fast_lo, fast_hi) only (e.g. not a neighbour's halo rows)
+    bool fast_piece = PEER ? fast && rb >= fast_lo && re <= fast_hi : fast;
+    // does this piece write rows a peer also receives (block-uniform)
+    bool mirror_piece = false;
+    for (int k = 0; PEER && k < mir.n; ++k) mirror_piece |= r0 < mir.m[k].row_hi && r1 > mir.m[k].row_lo;
+    mirrored |= mirror_piece;
+    if (PEER) {
+      if (mirror_piece && mir.sync_on) {
+        if (lane == 0) edge_wait(mir, err_flag);  // before any input row is fetched
+        __syncwarp();
+        // the bound now includes the neighbours' rows this piece reads
+        fast_piece = amax_in != nullptr && *(volatile const float*)amax_in < limit && rb >= fast_lo &&
+                     re <= fast_hi;
+      }
+    }
 
     // running source pointers of the next row to prefetch (row rb + t + D)
     const T* uf = ub + (int64_t)D * us;
@@ -899,10 +1002,10 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
     int t = 0;
     turns(std::integral_constant<int, kEdgeAll>{}, t, t1);
     if (col_edge) {
-      if (fast) turns(std::integral_constant<int, kCols | kFast>{}, t, t2);
+      if (fast_piece) turns(std::integral_constant<int, kCols | kFast>{}, t, t2);
       else turns(std::integral_constant<int, kCols>{}, t, t2);
     } else {
-      if (fast) turns(std::integral_constant<int, kFast>{}, t, t2);
+      if (fast_piece) turns(std::integral_constant<int, kFast>{}, t, t2);
       else turns(std::integral_constant<int, 0>{}, t, t2);
     }
     turns(std::integral_constant<int, kEdgeAll>{}, t, nfull);
@@ -910,12 +1013,39 @@ __global__ void __launch_bounds__(32 * WPB, FusedShape<KL, V>::kWarpsPerSm / WPB
     for (int sd = 0; sd < D; ++sd)
       if (nfull + sd < nrow) row(std::integral_constant<int, kEdgeAll>{}, AllLevels{}, nfull + sd, sd);
     cp_async_wait<0>();
+    if (PEER && mirror_piece && keep) {
+      // the piece's rows a peer also receives, re-read from what this lane
+      // just stored (same thread: program order) and written over NVLink
+      for (int k = 0; k < mir.n; ++k) {
+        const cq_mirror_t& m = mir.m[k];
+        for (int64_t r = max(r0, m.row_lo); r < min(r1, m.row_hi); ++r) {
+          const T* ll = (const T*)out_last.ptr + (col - out_last.alloc.lo[2]) + (r - out_last.alloc.lo[1]) * ls;
+          const T* lp = (const T*)out_prev.ptr + (col - out_prev.alloc.lo[2]) + (r - out_prev.alloc.lo[1]) * pstr;
+          *reinterpret_cast<Vec*>((T*)m.last + (r - m.row0) * m.stride + (col - m.col0)) = *reinterpret_cast<const Vec*>(ll);
+          *reinterpret_cast<Vec*>((T*)m.prev + (r - m.row0) * m.stride + (col - m.col0)) = *reinterpret_cast<const Vec*>(lp);
+        }
+      }
+    }
   }
   if (amax_out != nullptr) {
     // values are >= 0, so their int bit patterns order like the floats
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     if (lane == 0) atomicMax(reinterpret_cast<int*>(amax_out), __float_as_int(amax));
+    // the rows a neighbour receives also raise its bound for the next pass
+    // (before the completion signal it waits for)
+    if (PEER && mirrored && lane == 0)
+      for (int k = 0; k < 2; ++k)
+        if (mir.sync_on && mir.sync.peer_amax[k] != nullptr)
+          atomicMax_system(reinterpret_cast<int*>(mir.sync.peer_amax[k]), __float_as_int(amax));
+  }
+  if (PEER && mirrored) {
+    // the peer rows (and bounds) before the pass's completion signal
+    if (mir.sync_on) {
+      if (lane == 0) edge_done(mir);
+    } else {
+      __threadfence_system();
+    }
   }
 }
 
@@ -944,9 +1074,11 @@ static int fused_map() {
 template <typename T, int KL, int V, int D, int WPB>
 static int fused_geometry(int64_t rows, int64_t W, FusedGeometry* g) {
   constexpr int sw = 32 * V - 2 * KL;
-  auto kern = wave5_fused_kernel<T, KL, V, D, WPB>;
+  auto kern = wave5_fused_kernel<T, KL, V, D, WPB, false>;
+  auto kern_peer = wave5_fused_kernel<T, KL, V, D, WPB, true>;
   const int smem = WPB * D * 2 * 32 * V * (int)sizeof(T);
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CQ_CHECK_CUDA(cudaFuncSetAttribute(kern_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   // resident blocks per SM of this instantiation (same on every B200)
   static const int per_sm = [&] {
     int nb = 0;
@@ -996,11 +1128,33 @@ static int fused_geometry(int64_t rows, int64_t W, FusedGeometry* g) {
 template <typename T, int KL, int V, int D, int WPB>
 static int launch_fused(cudaStream_t st, const cq_view_t& u, const cq_view_t& upr, const cq_view_t& ol,
                         const cq_view_t& op, int64_t in_lo, int64_t in_hi, int64_t out_lo, int64_t out_hi,
-                        int64_t H, int64_t W, T c, const float* amax_in, float* amax_out, float limit) {
+                        int64_t H, int64_t W, T c, const float* amax_in, float* amax_out, float limit,
+                        int64_t fast_lo, int64_t fast_hi, FusedMirrors mir, unsigned long long* err_flag) {
   FusedGeometry g;
   CQ_TRY((fused_geometry<T, KL, V, D, WPB>(out_hi - out_lo, W, &g)));
-  wave5_fused_kernel<T, KL, V, D, WPB><<<(unsigned)g.blocks, g.threads, g.smem, st>>>(
-      u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, g.per_warp, g.map, amax_in, amax_out, limit);
+  if (mir.sync_on) {
+    // blocks (strip-minor pieces) whose rows meet a mirror range
+    CQ_REQUIRE(g.map == 2, "cq_wave5_fused_ex: peer sync needs the strip-minor layout");
+    const int64_t rows = out_hi - out_lo, pieces = (rows + g.per_warp - 1) / g.per_warp;
+    const int64_t strips = g.warps / pieces;
+    int64_t edge_pieces = 0;
+    for (int64_t q = 0; q < pieces; ++q) {
+      const int64_t a = out_lo + q * g.per_warp, b = std::min(out_hi, a + g.per_warp);
+      bool e = false;
+      for (int k = 0; k < mir.n; ++k) e |= a < mir.m[k].row_hi && b > mir.m[k].row_lo;
+      edge_pieces += e;
+    }
+    mir.n_edge = (int)(strips * edge_pieces);
+    if (mir.n_edge == 0) mir.sync_on = 0;
+  }
+  if (mir.n > 0)
+    wave5_fused_kernel<T, KL, V, D, WPB, true><<<(unsigned)g.blocks, g.threads, g.smem, st>>>(
+        u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, g.per_warp, g.map, amax_in, amax_out, limit, fast_lo,
+        fast_hi, mir, err_flag);
+  else
+    wave5_fused_kernel<T, KL, V, D, WPB, false><<<(unsigned)g.blocks, g.threads, g.smem, st>>>(
+        u, upr, ol, op, in_lo, in_hi, out_lo, out_hi, H, W, c, g.per_warp, g.map, amax_in, amax_out, limit, fast_lo,
+        fast_hi, mir, err_flag);
   return CQ_OK;
 }
 
@@ -1015,13 +1169,17 @@ struct FusedLaunch {
   float* amax_out;
   float limit;
   FusedGeometry* geometry;
+  int64_t fast_lo, fast_hi;
+  FusedMirrors mir;
+  unsigned long long* err_flag;
 };
 
 template <typename T, int KL, int V, int D, int WPB = 1>
 static int fused_run(const FusedLaunch& L) {
   if (L.geometry) return fused_geometry<T, KL, V, D, WPB>(L.out_hi - L.out_lo, L.W, L.geometry);
   return launch_fused<T, KL, V, D, WPB>(L.st, *L.u, *L.upr, *L.out_last, *L.out_prev, L.in_lo, L.in_hi, L.out_lo,
-                                        L.out_hi, L.H, L.W, (T)L.c, L.amax_in, L.amax_out, L.limit);
+                                        L.out_hi, L.H, L.W, (T)L.c, L.amax_in, L.amax_out, L.limit, L.fast_lo,
+                                        L.fast_hi, L.mir, L.err_flag);
 }
 
 // warps per block: CQ_FUSED_WPB (A/B sweeps; 1 = one-warp blocks)
@@ -1165,6 +1323,15 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
                            const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
                            int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4,
                            const float* amax_in, float* amax_out) {
+  return cq_wave5_fused_ex(device, stream, kind, levels, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi,
+                           extent, c, k2, k4, amax_in, amax_out, in_lo, in_hi, nullptr, 0, nullptr);
+}
+
+int cq_wave5_fused_ex(int device, int stream, int kind, int levels, const cq_view_t* u, const cq_view_t* upr,
+                      const cq_view_t* out_last, const cq_view_t* out_prev, int64_t in_lo, int64_t in_hi,
+                      int64_t out_lo, int64_t out_hi, const cq_box_t* extent, double c, double k2, double k4,
+                      const float* amax_in, float* amax_out, int64_t fast_lo, int64_t fast_hi,
+                      const cq_mirror_t* mirrors, int n_mirrors, const cq_peer_sync_t* sync) {
   CQ_GET_STREAM(device, stream);
   if (out_hi <= out_lo) return CQ_OK;
   const int64_t H = extent->hi[1], W = extent->hi[2];
@@ -1197,8 +1364,19 @@ int cq_wave5_fused_bounded(int device, int stream, int kind, int levels, const c
   const float limit = fast_ok && c > 0.0
                           ? (float)(std::ldexp(1.0, 124) / std::pow(3.0 + 8.0 * std::fabs(c) + 1e-3, levels))
                           : 0.f;
+  CQ_REQUIRE(n_mirrors >= 0 && n_mirrors <= 2 && (n_mirrors == 0 || mirrors != nullptr),
+             "cq_wave5_fused_ex: 0..2 mirrors");
+  FusedMirrors mir{};
+  for (int k = 0; k < n_mirrors; ++k) mir.m[k] = mirrors[k];
+  mir.n = n_mirrors;
+  if (sync != nullptr) {
+    CQ_REQUIRE(sync->count != nullptr && sync->done != nullptr && n_mirrors > 0,
+               "cq_wave5_fused_ex: peer sync needs counters and mirrors");
+    mir.sync = *sync;
+    mir.sync_on = 1;
+  }
   FusedLaunch L{st, u, upr, out_last, out_prev, in_lo, in_hi, out_lo, out_hi, H, W, c, k2, k4, amax_in, amax_out,
-                limit, nullptr};
+                limit, nullptr, fast_lo, fast_hi, mir, (unsigned long long*)ds->error_flag};
   CQ_TRY(fused_dispatch(kind, levels, L));
   CQ_CHECK_LAUNCH();
   return CQ_OK;
@@ -1221,6 +1399,26 @@ int cq_wave5_fused_geometry(int device, int kind, int levels, int64_t rows, int6
   out[1] = g.blocks;
   out[2] = g.warps;
   out[3] = g.computed_cells;
+  return CQ_OK;
+}
+
+int cq_p2p_wait(int device, int stream, const uint64_t* slot0, const uint64_t* slot1, const uint64_t* count,
+                int64_t timeout_ns) {
+  CQ_GET_STREAM(device, stream);
+  CQ_REQUIRE(count != nullptr, "cq_p2p_wait: null counter");
+  p2p_wait_kernel<<<1, 1, 0, st>>>((const unsigned long long*)slot0, (const unsigned long long*)slot1,
+                                   (const unsigned long long*)count, (long long)timeout_ns,
+                                   (unsigned long long*)ds->error_flag);
+  CQ_CHECK_LAUNCH();
+  return CQ_OK;
+}
+
+int cq_p2p_signal(int device, int stream, uint64_t* count, uint64_t* peer0, uint64_t* peer1) {
+  CQ_GET_STREAM(device, stream);
+  CQ_REQUIRE(count != nullptr, "cq_p2p_signal: null counter");
+  p2p_signal_kernel<<<1, 1, 0, st>>>((unsigned long long*)count, (unsigned long long*)peer0,
+                                     (unsigned long long*)peer1);
+  CQ_CHECK_LAUNCH();
   return CQ_OK;
 }
 

@@ -4,6 +4,7 @@
 // (pkg/src/clusterq/simulator.py:81-98 per-node storage, :166-193 push /
 // await-push payloads, :210-222 final gather) with HBM allocations, DMA
 // copies over PCIe / NVLink and NCCL point-to-point transfers.
+#include <cstring>
 #include <nccl.h>
 
 #include <map>
@@ -628,6 +629,30 @@ int cq_nccl_bcast(int device, int stream, void* buf, int64_t bytes, int root) {
   CQ_STREAM(device, stream);
   CQ_REQUIRE(g_comm && device == g_comm_device, "NCCL not initialised for device %d", device);
   CQ_CHECK_NCCL(ncclBroadcast(buf, buf, (size_t)bytes, ncclChar, root, g_comm, st));
+  return CQ_OK;
+}
+
+// ------------------------------------------------------------ CUDA IPC
+int cq_ipc_handle(const void* ptr, unsigned char handle_out[64]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  CQ_CHECK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+  memcpy(handle_out, &h, sizeof(h));
+  return CQ_OK;
+}
+
+int cq_ipc_open(int device, const unsigned char handle[64], void** ptr) {
+  CQ_TRY(ensure_device(device));
+  CQ_CHECK_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CQ_CHECK_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return CQ_OK;
+}
+
+int cq_ipc_close(int device, void* ptr) {
+  CQ_CHECK_CUDA(cudaSetDevice(device));
+  CQ_CHECK_CUDA(cudaIpcCloseMemHandle(ptr));
   return CQ_OK;
 }
 

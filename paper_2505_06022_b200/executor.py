@@ -140,7 +140,7 @@ class Placement:
 
 _dist_state = {"placement": None, "nccl": False}
 # counts of collective lowerings this process issued (tests / evidence)
-STATS = {"allgather": 0, "bcast": 0, "nccl_groups": 0, "h2d_bytes": 0, "upload_dedup_bytes": 0}
+STATS = {"allgather": 0, "bcast": 0, "nccl_groups": 0, "h2d_bytes": 0, "upload_dedup_bytes": 0, "peer_blocks": 0}
 
 
 def local_placement() -> Placement:
@@ -238,6 +238,8 @@ def _raise_flag(code, point):
         raise EvalError(f"integer division by zero at id {point}")
     if code == N.CQ_ERR_MAPPER:
         raise MapperViolationError(f"read at id {point} outside the mapped region")
+    if code == N.CQ_ERR_P2P:
+        raise NativeError(f"a neighbour's halo signal did not arrive (wanted pass {point[0]}, saw {point[1]})")
 
 
 def _memory_owner(arr):
@@ -371,6 +373,161 @@ class _View:
         return self.ptr + off * self.itemsize
 
 
+class _PeerView:
+    """A peer rank's allocation opened through CUDA IPC (device pointer valid
+    in this process): the ``c`` view of a copy destination, never freed here."""
+
+    __slots__ = ("ptr", "c")
+
+    def __init__(self, ptr, box):
+        lo, hi = _pad(box)
+        shape = [h - l for l, h in zip(lo, hi)]
+        self.ptr = ptr
+        v = N.CqView()
+        v.ptr = ptr
+        v.alloc.lo[:] = lo
+        v.alloc.hi[:] = hi
+        v.stride[:] = [shape[1] * shape[2], shape[2], 1]
+        self.c = v
+
+
+class _PeerHalo:
+    """The halo rows of a temporally blocked chain written straight into the
+    neighbouring ranks' allocations over NVLink, instead of one NCCL exchange
+    per block.  The NCCL exchange's kernel needs SM slots the running pass
+    holds, so it finished only as the pass drained and the edge launches ran
+    after it (~30 us per pass at N=2, ~60 at N=4; profiles/r02/
+    halo_timeline_n2.log).  Here, per block: wait until both neighbours have
+    finished the previous block (their rows for this block are in place, and
+    they no longer read the rows this block writes to them); one launch over
+    the whole slab; copy-engine copies of the KL rows next to each neighbour,
+    of both output fields, into that neighbour's output allocation (CUDA IPC
+    pointers); bump and publish this rank's pass counter.  The chain's first
+    block reads its halo through the plan's NCCL exchange as before."""
+
+    TIMEOUT_NS = 2_000_000_000   # a wait that long is a bug: the device flag reports it, the stream moves on
+
+    def __init__(self, sess, ch):
+        self.s = sess
+        me = self.me = sess.pl.rank
+        self.lo, self.hi = ch.rows[me]
+        self.top = next((n for n, (_l, h) in ch.rows.items() if h == self.lo), None)
+        self.bot = next((n for n, (l, _h) in ch.rows.items() if l == self.hi), None)
+        self.dev = sess.dev(me)
+        self.bufs = (ch.a, ch.b)
+        self.mine = {buf: (sess.views[(me, buf)], sess.alt[(me, buf)]) for buf in self.bufs}
+        # signal words: [0] written by the top neighbour, [1] by the bottom one, [2] this rank's pass count
+        p = ctypes.c_void_p()
+        N.call("cq_malloc", self.dev, 64, ctypes.byref(p))
+        self.sig = p.value
+        zero = np.zeros(8, np.uint64)
+        N.call("cq_copy_h2d", self.dev, N.STREAM_COMM, p, ctypes.c_void_p(zero.ctypes.data), 64)
+        N.call("cq_stream_synchronize", self.dev, N.STREAM_COMM)
+        # the per-block |X| bounds (float32 chains): edge blocks raise the
+        # neighbours' too, so every piece keeps the FMA form
+        self.amax = sess._amax.get((sess.chains.index(ch), me))
+        ptrs = [v.ptr for buf in self.bufs for v in self.mine[buf]] + [self.sig]
+        if self.amax is not None:
+            ptrs.append(self.amax)
+        blob = b"".join(self._handle(x) for x in ptrs)
+        table = sess.allgather_bytes(blob)
+        self.peer, self.opened = {}, []
+        for nbr in (self.top, self.bot):
+            if nbr is None:
+                continue
+            theirs = [self._open(table[nbr][64 * i:64 * (i + 1)]) for i in range(len(ptrs))]
+            entry = {}
+            for k, buf in enumerate(self.bufs):
+                box = sess._alloc_box[(nbr, buf)]
+                entry[buf] = (_PeerView(theirs[2 * k], box), _PeerView(theirs[2 * k + 1], box))
+            entry["sig"] = theirs[4]
+            entry["amax"] = theirs[5] if self.amax is not None else None
+            self.peer[nbr] = entry
+
+    def _handle(self, ptr):
+        h = (ctypes.c_ubyte * 64)()
+        N.call("cq_ipc_handle", ctypes.c_void_p(ptr), h)
+        return bytes(h)
+
+    def _open(self, handle):
+        p = ctypes.c_void_p()
+        N.call("cq_ipc_open", self.dev, (ctypes.c_ubyte * 64).from_buffer_copy(handle), ctypes.byref(p))
+        self.opened.append(p.value)
+        return p.value
+
+    def close(self):
+        for p in self.opened:
+            try:
+                N.call("cq_ipc_close", self.dev, ctypes.c_void_p(p))
+            except NativeError:
+                pass
+        self.opened = []
+        if self.sig:
+            N.call("cq_free", self.dev, ctypes.c_void_p(self.sig))
+            self.sig = None
+
+    def _halo_rows(self, kl, W, views):
+        """(view, halo-row region, write) of the rows the neighbours write."""
+        boxes = []
+        if self.top is not None:
+            boxes.append(Box((self.lo - kl, 0), (self.lo, W)))
+        if self.bot is not None:
+            boxes.append(Box((self.hi, 0), (self.hi + kl, W)))
+        if not boxes:
+            return []
+        reg = Region(2, boxes)
+        return [(v, reg, True) for v in views]
+
+    def wait(self, kl, W, views):
+        """Stream waits until both neighbours have finished as many blocks as
+        this rank; registered as a write of the halo rows the neighbours
+        write, so later local users of those rows order after it."""
+        s, dev, lane = self.s, self.dev, self.s.lane(self.me)
+        slot_t = ctypes.c_void_p(self.sig) if self.top is not None else None
+        slot_b = ctypes.c_void_p(self.sig + 8) if self.bot is not None else None
+
+        def go():
+            N.call("cq_p2p_wait", dev, lane, slot_t, slot_b, ctypes.c_void_p(self.sig + 16), self.TIMEOUT_NS)
+        return s.issue(dev, lane, self._halo_rows(kl, W, views), go)
+
+    def mirrors(self, depth, outs):
+        """cq_mirror_t array for the pass writing ``outs`` (X(t+KL), X(t+KL-1)):
+        the ``depth`` rows next to each neighbour also go to that neighbour's
+        output allocations (the same slot on every rank: lock-step swaps)."""
+        arr = (N.CqMirror * 2)()
+        n = 0
+        for nbr, (r0, r1) in ((self.top, (self.lo, self.lo + depth)), (self.bot, (self.hi - depth, self.hi))):
+            if nbr is None:
+                continue
+            dst = [self.peer[nbr][buf][0 if out is self.mine[buf][0] else 1] for buf, out in zip(self.bufs, outs)]
+            m = arr[n]
+            m.last, m.prev = dst[0].ptr, dst[1].ptr
+            m.row0, m.col0, m.stride = dst[0].c.alloc.lo[1], dst[0].c.alloc.lo[2], dst[0].c.stride[1]
+            m.row_lo, m.row_hi = r0, r1
+            n += 1
+        return arr, n
+
+    def sync(self, bi):
+        """cq_peer_sync_t of this rank's passes: the edge blocks wait for the
+        neighbours' counters (words [0] / [1] here) to reach this rank's count
+        (word [2]); the last edge block bumps it and stores it into the
+        neighbours' words ([1] of the top one, [0] of the bottom one); word
+        [3] counts the pass's finished edge blocks."""
+        sy = N.CqPeerSync()
+        if self.top is not None:
+            sy.slot[0] = self.sig
+            sy.peer_slot[0] = self.peer[self.top]["sig"] + 8
+        if self.bot is not None:
+            sy.slot[1] = self.sig + 8
+            sy.peer_slot[1] = self.peer[self.bot]["sig"]
+        sy.count, sy.done = self.sig + 16, self.sig + 24
+        for k, nbr in enumerate((self.top, self.bot)):
+            if nbr is not None and self.peer[nbr]["amax"] is not None:
+                sy.peer_amax[k] = self.peer[nbr]["amax"] + 4 * (bi + 1)   # their bound after block bi
+        sy.timeout_ns = self.TIMEOUT_NS
+        return sy
+
+
 # ------------------------------------------------------------- hazard tracker
 
 class _Hazards:
@@ -484,6 +641,7 @@ class Session:
         self._lanes = None      # node -> compute stream (lane())
         self._exec_of = None    # (task id, node) -> ExecuteCommand (exec_fused)
         self._jcols = None      # N-body j columns (cq_nbody_jcols)
+        self._peer = {}         # chain index -> _PeerHalo or None (peer-memory halo rows)
         self._halo_marks = []   # trace marks of a fused block's halo transfers
         self.t0 = None
         self._t0 = {}
@@ -609,6 +767,7 @@ class Session:
                     touch.setdefault((node, buf), []).append(
                         Box((max(lo - ch.depth, 0), 0), (min(hi + ch.depth, ch.H), ch.W)))
                     fused.add((node, buf))
+        self._alloc_box = {k: _bbox_union(v) for k, v in touch.items()}
         for (node, buf), boxes in sorted(touch.items()):
             if not self.local(node):
                 continue
@@ -1027,6 +1186,9 @@ class Session:
         kl = block.kl
         if hostinit:
             self.flush_group(hostinit)   # upload-time materialisation only
+        ph = self._peer_halo_for(ch)
+        if ph is not None:
+            return self._exec_fused_peer(ch, block, replaced, ph)
         b = self.buffers[ch.a]
         self._halo_marks = []
         self.flush_group(fusion.halo_pushes(ch, kl, b.itemsize))
@@ -1084,6 +1246,100 @@ class Session:
             if self.want_trace:
                 for i, tid in enumerate(block.tasks):
                     self.trace_marks.append((self._exec_of[(tid, node)], node, dev, marks, (i, kl)))
+
+    def _peer_halo_for(self, ch):
+        """The chain's _PeerHalo when its blocks' halo rows can go straight to
+        the neighbouring ranks (one node per rank, every rank in the chain,
+        CQ_WAVE_P2P not 0), else None; decided identically on every rank."""
+        ci = self.chains.index(ch)
+        if ci not in self._peer:
+            ok = (self.pl.world > 1 and self.nodes == self.pl.world and not self.capturing
+                  and os.environ.get("CQ_WAVE_P2P", "1") != "0"
+                  and getattr(N.load(), "supports_peer_memory", True)
+                  and set(ch.rows) == set(range(self.nodes)) and all(self.rank(n) == n for n in ch.rows))
+            self._peer[ci] = _PeerHalo(self, ch) if ok else None
+        return self._peer[ci]
+
+    def _exec_fused_peer(self, ch, block, replaced, ph):
+        """A fused block whose halo rows the neighbours wrote into this rank's
+        allocation (_PeerHalo): wait for them, one launch over the slab, then
+        write this rank's edge rows into the neighbours' output allocations."""
+        kl = block.kl
+        b = self.buffers[ch.a]
+        W, me, dev, lane = ch.W, ph.me, ph.dev, self.lane(ph.me)
+        ci, bi = self.chains.index(ch), ch.blocks.index(block)
+        ua, pb = self.views[(me, ch.a)], self.views[(me, ch.b)]
+        oa, ob = self.alt[(me, ch.a)], self.alt[(me, ch.b)]
+        marks = []
+        STATS["peer_blocks"] += 1
+        self._halo_marks = []
+        if bi == 0:
+            # the chain's first halo comes through the plan's exchange
+            self.flush_group(fusion.halo_pushes(ch, kl, b.itemsize))
+        lo, hi = ph.lo, ph.hi
+        in_lo = lo - kl if ph.top is not None else lo
+        in_hi = hi + kl if ph.bot is not None else hi
+        slots = self._amax.get((ci, me))
+        amax_out = None if slots is None else slots + 4 * (bi + 1)
+        amax_in = slots + 4 * bi if (slots is not None and bi > 0) else None
+        rin = Region.from_box(Box((in_lo, 0), (in_hi, W)))
+        rout = Region.from_box(Box((lo, 0), (hi, W)))
+        ext = _cbox(b.extent)
+        acc = [(ua, rin, False), (pb, rin, False), (oa, rout, True), (ob, rout, True)]
+        # the next block's halo (up to the chain's depth) goes to the neighbours
+        mir, nmir = ph.mirrors(ch.depth, (oa, ob))
+        sync = ph.sync(bi)
+
+        def go():
+            # the bound covers every row read: the neighbours raised it with
+            # the rows they sent before signalling (cq_peer_sync_t.peer_amax)
+            N.call("cq_wave5_fused_ex", dev, lane, N.KIND_CODE[b.element_kind], kl, ctypes.byref(ua.c),
+                   ctypes.byref(pb.c), ctypes.byref(oa.c), ctypes.byref(ob.c), in_lo, in_hi, lo, hi,
+                   ctypes.byref(ext), ctypes.c_double(ch.c), ctypes.c_double(ch.k2), ctypes.c_double(ch.k4),
+                   ctypes.c_void_p(amax_in), ctypes.c_void_p(amax_out), in_lo, in_hi, mir, nmir,
+                   ctypes.byref(sync))
+        t = self.issue(dev, lane, acc, go)
+        marks.append(t)
+        if self.want_trace:
+            self.launch_log.append((f"wave5_fused{kl}", (hi - lo) * W, dev, lane, t[0], t[1]))
+        pub = [t]
+        self.views[(me, ch.a)], self.alt[(me, ch.a)] = oa, ua
+        self.views[(me, ch.b)], self.alt[(me, ch.b)] = ob, pb
+        if block is ch.blocks[-1]:
+            # the neighbours' last rows into this rank land before anything
+            # else here touches the halo rows
+            pub.append(ph.wait(ch.depth, W, (oa, ob, ua, pb)))
+        if self.want_trace:
+            if self._exec_of is None:
+                self._exec_of = {(c.task_id, c.node): c for c in self.plan.commands
+                                 if isinstance(c, ExecuteCommand)}
+            for p in replaced:
+                if me not in (p.src, p.dst):
+                    continue
+                hm = next(((st, sp) for hp, node, _d, st, sp in self._halo_marks
+                           if (hp.src, hp.dst) == (p.src, p.dst)), None)
+                start, stop = hm if hm is not None else ((pub[0][0], pub[-1][1]) if p.src == me else marks[0])
+                self.trace_marks.append((p, me, dev, start, stop))
+            for i, tid in enumerate(block.tasks):
+                self.trace_marks.append((self._exec_of[(tid, me)], me, dev, marks + pub, (i, kl)))
+
+    def allgather_bytes(self, blob: bytes):
+        """Every rank's ``blob`` (equal lengths), through one NCCL all-gather."""
+        n, world, me = len(blob), self.pl.world, self.pl.rank
+        dev = self.pl.devices[0]
+        p = ctypes.c_void_p()
+        N.call("cq_malloc", dev, n * world, ctypes.byref(p))
+        host = np.frombuffer(blob, dtype=np.uint8).copy()
+        out = np.empty(n * world, dtype=np.uint8)
+        try:
+            N.call("cq_copy_h2d", dev, N.STREAM_COMM, ctypes.c_void_p(p.value + me * n),
+                   ctypes.c_void_p(host.ctypes.data), n)
+            N.call("cq_nccl_allgather", dev, N.STREAM_COMM, ctypes.c_void_p(p.value + me * n), p, n)
+            N.call("cq_copy_d2h", dev, N.STREAM_COMM, ctypes.c_void_p(out.ctypes.data), p, n * world)
+            N.call("cq_stream_synchronize", dev, N.STREAM_COMM)
+        finally:
+            N.call("cq_free", dev, p)
+        return [out[k * n:(k + 1) * n].tobytes() for k in range(world)]
 
     def exec_kick(self, task, cmd, binding, got, dev, lane, rviews, wviews):
         """The N-body kick of a chunk whose 'all'-mapped positions are partly
@@ -1602,6 +1858,10 @@ class Session:
                 except NativeError:
                     pass
         self._drop_graph()
+        for ph in self._peer.values():
+            if ph is not None:
+                ph.close()
+        self._peer = {}
         self.release()
         if self._flag_host is not None:
             N.call("cq_host_free", self._flag_host)

@@ -123,6 +123,29 @@ def main():
             err = np.abs(res.buffers["C"][rows] - c) / cabs
             check(f"sgemm {variant} {m}x{nn}x{k} err={err.max():.2e}", err.max() <= 1e-6)
 
+    # fused chain across ranks with peer-memory halo rows (CUDA IPC + NVLink
+    # copies, device pass counters): a run, then a captured graph replayed
+    # twice continuing the simulation on the device
+    before = E.STATS["peer_blocks"]
+    prog = W.wave_program(h, w, steps=22, kind="float32", u0=u0, up0=up0)
+    sess = E.Session(cq.generate_commands(prog.graph(), world), pl)
+    sess.execute(upload=True)
+    sess.synchronize()
+    first = sess.results()
+    sess.recycle()
+    sess.capture()
+    sess.replay(2)
+    sess.synchronize()
+    again = sess.results()
+    sess.close()
+    if rank == 0:
+        u1, up1 = onat.wave_run(u0, up0, 22, 0.25)
+        u3, up3 = onat.wave_run(u0, up0, 66, 0.25)
+        used = E.STATS["peer_blocks"] - before
+        check(f"wave fused nodes={world} peer-memory halo rows ({used} blocks), run + 2 graph replays",
+              (used > 0 or world == 1) and dsl.same_bits(first["u"], u1) and dsl.same_bits(first["up"], up1)
+              and dsl.same_bits(again["u"], u3) and dsl.same_bits(again["up"], up3))
+
     # one node's row pushed to every other node: one in-place ncclBroadcast
     before = E.STATS["bcast"]
     res = E.run(cq.generate_commands(W.row_broadcast_program(4 * world).graph(), world), placement=pl)

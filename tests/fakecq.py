@@ -27,6 +27,10 @@ def _obj(x):
 
 
 class FakeLib:
+    # no CUDA IPC between the gloo test processes: fused chains across ranks
+    # take the NCCL halo exchange (the peer-memory path is covered on GPUs)
+    supports_peer_memory = False
+
     def __init__(self, ndev=1, transport=None):
         self.ndev = ndev
         self.blocks = {}      # base -> np.uint8 array
