@@ -429,20 +429,34 @@ class _PeerHalo:
         ptrs = [v.ptr for buf in self.bufs for v in self.mine[buf]] + [self.sig]
         if self.amax is not None:
             ptrs.append(self.amax)
-        blob = b"".join(self._handle(x) for x in ptrs)
-        table = sess.allgather_bytes(blob)
         self.peer, self.opened = {}, []
-        for nbr in (self.top, self.bot):
-            if nbr is None:
-                continue
-            theirs = [self._open(table[nbr][64 * i:64 * (i + 1)]) for i in range(len(ptrs))]
-            entry = {}
-            for k, buf in enumerate(self.bufs):
-                box = sess._alloc_box[(nbr, buf)]
-                entry[buf] = (_PeerView(theirs[2 * k], box), _PeerView(theirs[2 * k + 1], box))
-            entry["sig"] = theirs[4]
-            entry["amax"] = theirs[5] if self.amax is not None else None
-            self.peer[nbr] = entry
+        # every step below is collective: a rank that cannot export or open
+        # IPC handles says so, and then every rank falls back together
+        try:
+            blob = b"\x01" + b"".join(self._handle(x) for x in ptrs)
+        except NativeError:
+            blob = b"\x00" * (1 + 64 * len(ptrs))
+        table = sess.allgather_bytes(blob)
+        ok = all(t[0] == 1 for t in table)
+        if ok:
+            try:
+                for nbr in (self.top, self.bot):
+                    if nbr is None:
+                        continue
+                    theirs = [self._open(table[nbr][1 + 64 * i:1 + 64 * (i + 1)]) for i in range(len(ptrs))]
+                    entry = {}
+                    for k, buf in enumerate(self.bufs):
+                        box = sess._alloc_box[(nbr, buf)]
+                        entry[buf] = (_PeerView(theirs[2 * k], box), _PeerView(theirs[2 * k + 1], box))
+                    entry["sig"] = theirs[4]
+                    entry["amax"] = theirs[5] if self.amax is not None else None
+                    self.peer[nbr] = entry
+            except NativeError:
+                ok = False
+            ok = all(t == b"\x01" for t in sess.allgather_bytes(b"\x01" if ok else b"\x00"))
+        self.ok = ok
+        if not ok:
+            self.close()
 
     def _handle(self, ptr):
         h = (ctypes.c_ubyte * 64)()
@@ -1257,7 +1271,8 @@ class Session:
                   and os.environ.get("CQ_WAVE_P2P", "1") != "0"
                   and getattr(N.load(), "supports_peer_memory", True)
                   and set(ch.rows) == set(range(self.nodes)) and all(self.rank(n) == n for n in ch.rows))
-            self._peer[ci] = _PeerHalo(self, ch) if ok else None
+            ph = _PeerHalo(self, ch) if ok else None
+            self._peer[ci] = ph if ph is not None and ph.ok else None
         return self._peer[ci]
 
     def _exec_fused_peer(self, ch, block, replaced, ph):
