@@ -12,7 +12,9 @@ pass by ``cq_wave5_fused`` instead of one ``cq_wave5`` launch per step:
 * the interior rows [lo+KL, hi-KL) depend only on the node's own rows and
   launch at once; the KL rows next to a neighbour need the neighbour's KL
   nearest rows of X(t) and X(t-1), exchanged once per block (NCCL / DMA,
-  through the executor's ordinary transfer path) while the interior runs;
+  through the executor's ordinary transfer path) while the interior runs --
+  or, with one node per rank, stored into the neighbour's memory by the
+  previous block's pass itself (executor._PeerHalo, one launch per block);
 * each cell is the same DSL tree with the same operands as the per-step
   execution, so results are bit-identical (tests/test_gpu_parity.py).
 

@@ -271,8 +271,8 @@ def test_fused_wave_chain_fast_form_signed_zeros(c):
 def test_fused_wave_graph_replay_continues_the_simulation():
     """A captured fused execution replayed twice == two more plain fused
     executions == the 3x-longer simulation (the KL-row exchange makes a
-    re-execution on resident data a true continuation; an even number of
-    out-of-place blocks keeps the captured pointers valid)."""
+    re-execution on resident data a true continuation; with an odd number of
+    out-of-place blocks the capture holds two alternating graphs)."""
     from paper_2505_06022_b200.executor import Placement, Session
     h, w, steps = 384, 512, 26
     u0 = np.random.default_rng(23).uniform(0, 1, (h, w)).astype(np.float32)
