@@ -139,6 +139,8 @@ class Placement:
 
 
 _dist_state = {"placement": None, "nccl": False}
+# page-locked error-flag read-back buffers of closed sessions, by size (reused: never freed)
+_FLAG_HOST_CACHE = {}
 # counts of collective lowerings this process issued (tests / evidence)
 STATS = {"allgather": 0, "bcast": 0, "nccl_groups": 0, "h2d_bytes": 0, "upload_dedup_bytes": 0, "peer_blocks": 0}
 
@@ -1879,7 +1881,9 @@ class Session:
         self._peer = {}
         self.release()
         if self._flag_host is not None:
-            N.call("cq_host_free", self._flag_host)
+            # back to the process-wide cache: cudaFreeHost measured 10-370 ms
+            # per call, inside run_batch's timed region
+            _FLAG_HOST_CACHE.setdefault(self._flag_host_bytes, []).append(self._flag_host)
             self._flag_host = None
         for pool in self.free_events.values():
             for ev in pool:
@@ -1904,9 +1908,14 @@ class Session:
         (``finish_results`` decodes it): a blocking read would wait for the
         copy engines, i.e. for the transfers of other runs in flight."""
         if self._flag_host is None:
-            ptr = ctypes.c_void_p()
-            N.call("cq_host_alloc", 32 * len(self.devices), ctypes.byref(ptr))
-            self._flag_host = ptr
+            nbytes = 32 * len(self.devices)
+            cached = _FLAG_HOST_CACHE.get(nbytes)
+            if cached:
+                ptr = cached.pop()
+            else:
+                ptr = ctypes.c_void_p()
+                N.call("cq_host_alloc", nbytes, ctypes.byref(ptr))
+            self._flag_host, self._flag_host_bytes = ptr, nbytes
         base = self._flag_host.value
         for k, d in enumerate(self.devices):
             N.call("cq_error_flag_async", d, self.d2h_stream, ctypes.c_void_p(base + 32 * k))
