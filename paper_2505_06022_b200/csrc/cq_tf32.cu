@@ -557,6 +557,16 @@ __global__ void split_rows_kernel(const float* __restrict__ a, int64_t lda, floa
   }
 }
 
+// A [m,k] dense -> lo only: the tensor core reads fp32 operands as TF32 by
+// dropping the low 13 mantissa bits, so A itself is its hi part (checked
+// bit for bit against the masked copy: tests/test_gpu_parity.py)
+__global__ void split_lo_kernel(const float* __restrict__ a, float* __restrict__ lo, int64_t total) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const float x = a[t];
+    lo[t] = x - tf32_hi(x);
+  }
+}
+
 // B [k,n] (ldb) -> hi, lo transposed [n,k] dense, via 32x32 shared tiles
 __global__ void split_transpose_kernel(const float* __restrict__ b, int64_t ldb, float* __restrict__ hi,
                                        float* __restrict__ lo, int64_t k, int64_t n) {
@@ -684,15 +694,22 @@ int sgemm_3xtf32(int device, int stream, cudaStream_t st, int sm_count, const fl
   (void)sm_count;
   CQ_REQUIRE(k % 4 == 0, "3xTF32 sgemm needs k %% 4 == 0 (16-byte TMA row pitch)");
   CQ_REQUIRE(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), "3xTF32 sgemm: dims exceed int32");
-  // scratch for the split operands: 2*(m+n)*k floats, reused across calls
+  // scratch for the split operands, reused across calls: A_lo, Bt_hi, Bt_lo
+  // ((m + 2n) k floats) when A is dense and serves as its own hi part (the
+  // MMA truncates to TF32), else A_hi as well (2 (m + n) k floats)
+  const char* rawv = getenv("CQ_TF32_RAW_HI");
+  const bool raw_hi = lda == k && !(rawv && rawv[0] == '0');
   float* scratch = nullptr;
-  size_t bytes = (size_t)2 * (size_t)(m + n) * (size_t)k * sizeof(float);
+  size_t bytes = (size_t)((raw_hi ? 1 : 2) * m + 2 * n) * (size_t)k * sizeof(float);
   CQ_TRY(cq::scratch(device, stream, 0, bytes, (void**)&scratch));
-  float* ahi = scratch;
-  float* alo = ahi + m * k;
+  const float* ahi = raw_hi ? a : scratch;
+  float* alo = raw_hi ? scratch : scratch + m * k;
   float* bhi = alo + m * k;
   float* blo = bhi + n * k;
-  tf32::split_rows_kernel<<<sm_count * 8, 256, 0, st>>>(a, lda, ahi, alo, m, k);
+  if (raw_hi)
+    tf32::split_lo_kernel<<<sm_count * 8, 256, 0, st>>>(a, alo, m * k);
+  else
+    tf32::split_rows_kernel<<<sm_count * 8, 256, 0, st>>>(a, lda, scratch, alo, m, k);
   CQ_CHECK_LAUNCH();
   dim3 tg((unsigned)((n + 31) / 32), (unsigned)((k + 31) / 32));
   tf32::split_transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(b, ldb, bhi, blo, k, n);

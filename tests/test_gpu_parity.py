@@ -347,6 +347,33 @@ def test_sgemm_within_tolerance(variant, nodes):
     assert err.max() <= 1e-6, err.max()
 
 
+@pytest.mark.parametrize("shape", [(512, 384, 256), (256, 512, 1024), (1000, 768, 2048)])
+def test_tf32_raw_a_is_its_own_hi_part(shape, monkeypatch):
+    """3xTF32 with A itself as the hi operand (the MMA drops the low 13
+    mantissa bits) gives the same C bits as the explicitly masked copy."""
+    import ctypes
+    import torch
+    from paper_2505_06022_b200 import _native as N
+    N.call("cq_init_device", 0)
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.rand((m, k), device="cuda", generator=g) * 2 - 1
+    b = torch.rand((k, n), device="cuda", generator=g) * 2 - 1
+    out = []
+    for raw in ("1", "0"):
+        monkeypatch.setenv("CQ_TF32_RAW_HI", raw)
+        c = torch.full((m, n), float("nan"), device="cuda")
+        torch.cuda.synchronize()
+        N.call("cq_sgemm", 0, 0, 1, ctypes.c_void_p(a.data_ptr()), k, ctypes.c_void_p(b.data_ptr()), n,
+               ctypes.c_void_p(c.data_ptr()), n, m, n, k)
+        N.call("cq_stream_synchronize", 0, 0)
+        out.append(c.cpu().numpy())
+    assert dsl.same_bits(out[0], out[1])
+    ref = a.double().cpu().numpy() @ b.double().cpu().numpy()
+    cabs = np.abs(a.double().cpu().numpy()) @ np.abs(b.double().cpu().numpy())
+    assert (np.abs(out[0] - ref) / cabs).max() <= 1e-6
+
+
 def test_fused_pass_rejects_bad_arguments():
     """The C-ABI fails loudly (NativeError with the reason) on arguments the
     fused pass cannot honour, instead of computing something else."""
