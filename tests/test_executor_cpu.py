@@ -638,6 +638,11 @@ def _rank_bcast_main(rank, world, port, outdir):
     N._lib = lib
     plan = cq.generate_commands(W.row_broadcast_program(4 * world).graph(), world)
     res = E.run(plan, placement=E.Placement(world, rank, (0,)))
+    # the byte all-gather the peer-memory setup uses (one NCCL all-gather)
+    sess = E.Session(plan, E.Placement(world, rank, (0,)))
+    blobs = sess.allgather_bytes(bytes([rank]) * 64)
+    sess.close()
+    assert blobs == [bytes([k]) * 64 for k in range(world)]
     n_b = sum(1 for x in lib.launches if isinstance(x, tuple) and x[0] == "bcast")
     n_g = sum(1 for x in lib.launches if isinstance(x, tuple) and x[0] == "group")
     np.savez(os.path.join(outdir, f"rank{rank}.npz"), d=res.buffers.get("d", np.zeros(0)), n=np.array([n_b, n_g]))
