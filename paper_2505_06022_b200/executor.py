@@ -407,7 +407,7 @@ class _PeerHalo:
     pointers); bump and publish this rank's pass counter.  The chain's first
     block reads its halo through the plan's NCCL exchange as before."""
 
-    TIMEOUT_NS = 2_000_000_000   # a wait that long is a bug: the device flag reports it, the stream moves on
+    TIMEOUT_NS = 30_000_000_000   # a wait that long is a bug (or a stalled rank): the device flag reports it
 
     def __init__(self, sess, ch):
         self.s = sess
