@@ -399,13 +399,17 @@ class _PeerHalo:
     per block.  The NCCL exchange's kernel needs SM slots the running pass
     holds, so it finished only as the pass drained and the edge launches ran
     after it (~30 us per pass at N=2, ~60 at N=4; profiles/r02/
-    halo_timeline_n2.log).  Here, per block: wait until both neighbours have
-    finished the previous block (their rows for this block are in place, and
-    they no longer read the rows this block writes to them); one launch over
-    the whole slab; copy-engine copies of the KL rows next to each neighbour,
-    of both output fields, into that neighbour's output allocation (CUDA IPC
-    pointers); bump and publish this rank's pass counter.  The chain's first
-    block reads its halo through the plan's NCCL exchange as before."""
+    halo_timeline_n2.log).  Here every block is one launch over the whole
+    slab (cq_wave5_fused_ex with cq_mirror_t / cq_peer_sync_t): the pieces
+    next to a neighbour first wait, in the kernel, until that neighbour has
+    finished the previous block (its rows for this block are in place, and it
+    no longer reads the rows this block sends it), and at their end store
+    their rows next to the neighbour, of both output fields, into the
+    neighbour's output allocation (CUDA IPC pointers, NVLink), raise its |X|
+    bound, and the last of them bumps and publishes this rank's pass counter.
+    Interior pieces never wait.  The chain's first block reads its halo
+    through the plan's NCCL exchange as before; a trailing cq_p2p_wait orders
+    the neighbours' last rows before anything else touches the halo rows."""
 
     TIMEOUT_NS = 30_000_000_000   # a wait that long is a bug (or a stalled rank): the device flag reports it
 
@@ -418,7 +422,8 @@ class _PeerHalo:
         self.dev = sess.dev(me)
         self.bufs = (ch.a, ch.b)
         self.mine = {buf: (sess.views[(me, buf)], sess.alt[(me, buf)]) for buf in self.bufs}
-        # signal words: [0] written by the top neighbour, [1] by the bottom one, [2] this rank's pass count
+        # signal words: [0] written by the top neighbour, [1] by the bottom one, [2] this rank's pass
+        # count, [3] the pass's finished edge blocks
         p = ctypes.c_void_p()
         N.call("cq_malloc", self.dev, 64, ctypes.byref(p))
         self.sig = p.value
