@@ -9,8 +9,9 @@
 // stays ~1e-8, where plain 1xTF32 (~5e-6 at K = 16384) fails the 1e-6 bar.
 //
 // Structure (one CTA per 128 x BN output tile, 1 CTA / SM):
-//   split pass : A -> A_hi, A_lo ([m,k], K-major); B -> Bt_hi, Bt_lo ([n,k],
-//                transposed to K-major), one HBM pass each;
+//   split pass : A -> A_lo ([m,k], K-major; A is its own hi operand); B ->
+//                B_lo ([k,n]; B its own hi, read MN-major by the CTA-pair
+//                kernel) or Bt_hi, Bt_lo ([n,k], transposed to K-major);
 //   warp 0     : TMA producer, 4 tiles (A_hi, A_lo, B_hi, B_lo) per 32-wide k
 //                block into a STAGES-deep ring, 128-byte swizzle;
 //   warp 1     : TMEM allocator + single-thread tcgen05.mma issuer,
@@ -86,11 +87,33 @@ __device__ __forceinline__ uint64_t smem_desc(const void* tile) {
   return d;
 }
 
-// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, K-major both.
-__host__ __device__ constexpr uint32_t instr_desc(int m, int n) {
+// MN-major operand tile straight from a row-major [k, n] matrix: 32-column
+// chunks (128 B per k row) one TMA box each, BK rows deep, in the 128-byte
+// swizzle with 32-byte atoms (the only MN-major smem layout kind::tf32 takes:
+// 4 k rows x 128 B, 32-byte chunks XORed with k % 4).  LBO = the distance
+// between n chunks (one box, BK * 128 B), SBO = between 4-row k groups
+// (512 B); layout type 1 = SWIZZLE_128B_BASE32B.  The encoding was pinned
+// on one MMA against a CPU product (scripts/r02/micro/umma_mn.cu,
+// profiles/r02/tf32_mn_major_descriptor_micro.log).
+template <int BK>
+__device__ __forceinline__ uint64_t smem_desc_mn(const void* tile) {
+  uint64_t addr = smem_u32(tile);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;            // start address      [0,14)
+  d |= (uint64_t)((BK * 128) >> 4) << 16;   // LBO: n chunk       [16,30)
+  d |= (uint64_t)(512 >> 4) << 32;          // SBO: 4-row k group [32,46)
+  d |= (uint64_t)1 << 46;                   // version            [46,48)
+  d |= (uint64_t)1 << 61;                   // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: F32 accumulate, TF32 A/B, A K-major,
+// B K-major or (b_mn) MN-major.
+__host__ __device__ constexpr uint32_t instr_desc(int m, int n, bool b_mn = false) {
   return (1u << 4)                    // c_format = F32
          | (2u << 7)                  // a_format = TF32
          | (2u << 10)                 // b_format = TF32
+         | (b_mn ? (1u << 16) : 0u)   // b_major = MN
          | ((uint32_t)(n >> 3) << 17)  // N >> 3
          | ((uint32_t)(m >> 4) << 24); // M >> 4
 }
@@ -398,7 +421,9 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
       : "memory");
 }
 
-template <int BN, int STAGES, int BK>
+// MNB: B hi / lo are read MN-major straight from [k, n] (BN / 64 boxes of 32
+// columns per CTA) instead of from the transposed [n, k] copies.
+template <int BN, int STAGES, int BK, bool MNB>
 __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
     sgemm_3xtf32_2sm_kernel(const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                             const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -459,15 +484,24 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
         const int kc = kb * BK;
         tma_load_2d_pair(S.a_hi[s], &map_ahi, bar, kc, row0);
         tma_load_2d_pair(S.a_lo[s], &map_alo, bar, kc, row0);
-        tma_load_2d_pair(S.b_hi[s], &map_bhi, bar, kc, col0 + (int)crank * (BN / 2));
-        tma_load_2d_pair(S.b_lo[s], &map_blo, bar, kc, col0 + (int)crank * (BN / 2));
+        if constexpr (MNB) {
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) {
+            const int cn = col0 + (int)crank * (BN / 2) + 32 * j;
+            tma_load_2d_pair(S.b_hi[s] + j * 32 * BK, &map_bhi, bar, cn, kc);
+            tma_load_2d_pair(S.b_lo[s] + j * 32 * BK, &map_blo, bar, cn, kc);
+          }
+        } else {
+          tma_load_2d_pair(S.b_hi[s], &map_bhi, bar, kc, col0 + (int)crank * (BN / 2));
+          tma_load_2d_pair(S.b_lo[s], &map_blo, bar, kc, col0 + (int)crank * (BN / 2));
+        }
       }
       // every multicast commit on this CTA's stage barriers has landed
       for (int kb = num_kb; kb < num_kb + STAGES; ++kb) mbar_wait(&S.empty[kb % STAGES], ((kb / STAGES) & 1) ^ 1);
     }
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {
-      constexpr uint32_t idesc = instr_desc(2 * BM, BN);
+      constexpr uint32_t idesc = instr_desc(2 * BM, BN, MNB);
       int kb = 0;
       for (int g = 0; g < num_groups; ++g) {
         const int buf = g & 1;
@@ -480,13 +514,15 @@ __global__ void __launch_bounds__(Epi<BN>::kThreads, 1)
           mbar_wait(&S.full[s], (kb / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t dah = smem_desc<BK>(S.a_hi[s]), dal = smem_desc<BK>(S.a_lo[s]);
-          const uint64_t dbh = smem_desc<BK>(S.b_hi[s]), dbl = smem_desc<BK>(S.b_lo[s]);
+          const uint64_t dbh = MNB ? smem_desc_mn<BK>(S.b_hi[s]) : smem_desc<BK>(S.b_hi[s]);
+          const uint64_t dbl = MNB ? smem_desc_mn<BK>(S.b_lo[s]) : smem_desc<BK>(S.b_lo[s]);
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint64_t o = (uint64_t)(kk * 2);
-            mma_tf32_pair(acc_addr, dah + o, dbh + o, idesc, (kb != first_kb || kk != 0) ? 1u : 0u);
-            mma_tf32_pair(acc_addr, dah + o, dbl + o, idesc, 1);
-            mma_tf32_pair(acc_addr, dal + o, dbh + o, idesc, 1);
+            const uint64_t o = (uint64_t)(kk * 2);             // 8 k = 32 B along a K-major row
+            const uint64_t ob = MNB ? (uint64_t)(kk * 64) : o;  // 8 k rows = 1 KB of MN-major rows
+            mma_tf32_pair(acc_addr, dah + o, dbh + ob, idesc, (kb != first_kb || kk != 0) ? 1u : 0u);
+            mma_tf32_pair(acc_addr, dah + o, dbl + ob, idesc, 1);
+            mma_tf32_pair(acc_addr, dal + o, dbh + ob, idesc, 1);
           }
           mma_commit_pair(&S.empty[s]);
         }
@@ -567,6 +603,16 @@ __global__ void split_lo_kernel(const float* __restrict__ a, float* __restrict__
   }
 }
 
+// B [k,n] (ldb) -> lo [k,n] dense, for the MN-major path (B is its own hi)
+__global__ void split_lo_rows_kernel(const float* __restrict__ b, int64_t ldb, float* __restrict__ lo, int64_t k,
+                                     int64_t n) {
+  const int64_t total = k * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const float x = b[(t / n) * ldb + t % n];
+    lo[t] = x - tf32_hi(x);
+  }
+}
+
 // B [k,n] (ldb) -> hi, lo transposed [n,k] dense, via 32x32 shared tiles
 __global__ void split_transpose_kernel(const float* __restrict__ b, int64_t ldb, float* __restrict__ hi,
                                        float* __restrict__ lo, int64_t k, int64_t n) {
@@ -600,19 +646,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-// 2-D row-major fp32 [rows, cols] (cols contiguous), box = [bk cols, box_rows].
-static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows, int bk) {
+// 2-D row-major fp32 [rows, cols] (cols contiguous, row pitch ld), box = [bk
+// cols, box_rows]; swizzle 128 B (bk 32) / 64 B (bk 16), or 128 B with
+// 32-byte atoms for the MN-major B boxes (atom32).
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int box_rows, int bk,
+                    int64_t ld = 0, bool atom32 = false) {
   auto encode = get_encode();
   if (!encode) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return CQ_ERR_CUDA;
   }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld ? ld : cols) * sizeof(float)};
   cuuint32_t box[2] = {(cuuint32_t)bk, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                             : (bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -653,16 +705,24 @@ static int launch(cudaStream_t st, const float* ahi, const float* alo, const flo
   return CQ_OK;
 }
 
-template <int BN, int STAGES, int BK>
-static int launch_2sm(cudaStream_t st, const float* ahi, const float* alo, const float* bhi, const float* blo,
-                      float* c, int64_t ldc, int64_t m, int64_t n, int64_t k) {
+// MNB: bhi is B itself ([k, n], row pitch ldb) and blo its dense [k, n] lo
+// part; otherwise both are the transposed [n, k] copies.
+template <int BN, int STAGES, int BK, bool MNB>
+static int launch_2sm(cudaStream_t st, const float* ahi, const float* alo, const float* bhi, int64_t ldb,
+                      const float* blo, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k) {
   CUtensorMap ma, mal, mb, mbl;
   CQ_TRY(make_map(&ma, ahi, m, k, BM, BK));
   CQ_TRY(make_map(&mal, alo, m, k, BM, BK));
-  CQ_TRY(make_map(&mb, bhi, n, k, BN / 2, BK));
-  CQ_TRY(make_map(&mbl, blo, n, k, BN / 2, BK));
+  if constexpr (MNB) {
+    static_assert(BK == 32, "MN-major B boxes are 32 columns x BK rows");
+    CQ_TRY(make_map(&mb, bhi, k, n, BK, 32, ldb, true));
+    CQ_TRY(make_map(&mbl, blo, k, n, BK, 32, n, true));
+  } else {
+    CQ_TRY(make_map(&mb, bhi, n, k, BN / 2, BK));
+    CQ_TRY(make_map(&mbl, blo, n, k, BN / 2, BK));
+  }
   size_t smem = sizeof(Smem2<BN, STAGES, BK>) + 1024;
-  auto kern = sgemm_3xtf32_2sm_kernel<BN, STAGES, BK>;
+  auto kern = sgemm_3xtf32_2sm_kernel<BN, STAGES, BK, MNB>;
   CQ_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int pairs_m = (int)((m + 2 * BM - 1) / (2 * BM));
   const int tiles_n = (int)((n + BN - 1) / BN);
@@ -694,13 +754,27 @@ int sgemm_3xtf32(int device, int stream, cudaStream_t st, int sm_count, const fl
   (void)sm_count;
   CQ_REQUIRE(k % 4 == 0, "3xTF32 sgemm needs k %% 4 == 0 (16-byte TMA row pitch)");
   CQ_REQUIRE(m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31), "3xTF32 sgemm: dims exceed int32");
-  // scratch for the split operands, reused across calls: A_lo, Bt_hi, Bt_lo
-  // ((m + 2n) k floats) when A is dense and serves as its own hi part (the
-  // MMA truncates to TF32), else A_hi as well (2 (m + n) k floats)
+  const char* bn = getenv("CQ_TF32_BN");
+  const char* mc = getenv("CQ_TF32_MC");
+  const char* bkv = getenv("CQ_TF32_BK");
+  bool wide = n >= 256 && !(bn && atoi(bn) == 128);
+  bool multicast = !(mc && atoi(mc) == 1);
+  bool bk16 = bkv && atoi(bkv) == 16;
+  const char* pair = getenv("CQ_TF32_2SM");
+  bool two_sm = wide && !(pair && atoi(pair) == 0);
+  // The CTA-pair kernel reads B MN-major straight from [k, n] when its rows
+  // are 16-byte aligned (TMA pitch): B itself is the hi operand and the
+  // split pass writes only its lo part, untransposed.
+  const char* mnbv = getenv("CQ_TF32_MNB");
+  const bool mnb = two_sm && !(mnbv && mnbv[0] == '0') && ldb % 4 == 0 && n % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+  // scratch for the split operands, reused across calls: A_lo [m,k] (A is its
+  // own hi part when dense -- the MMA truncates to TF32 -- else A_hi as
+  // well), then B_lo [k,n] (MN-major path) or Bt_hi, Bt_lo [n,k]
   const char* rawv = getenv("CQ_TF32_RAW_HI");
   const bool raw_hi = lda == k && !(rawv && rawv[0] == '0');
   float* scratch = nullptr;
-  size_t bytes = (size_t)((raw_hi ? 1 : 2) * m + 2 * n) * (size_t)k * sizeof(float);
+  size_t bytes = (size_t)((raw_hi ? 1 : 2) * m + (mnb ? 1 : 2) * n) * (size_t)k * sizeof(float);
   CQ_TRY(cq::scratch(device, stream, 0, bytes, (void**)&scratch));
   const float* ahi = raw_hi ? a : scratch;
   float* alo = raw_hi ? scratch : scratch + m * k;
@@ -711,20 +785,21 @@ int sgemm_3xtf32(int device, int stream, cudaStream_t st, int sm_count, const fl
   else
     tf32::split_rows_kernel<<<sm_count * 8, 256, 0, st>>>(a, lda, scratch, alo, m, k);
   CQ_CHECK_LAUNCH();
+  if (mnb) {
+    float* blo_kn = alo + m * k;
+    if (ldb == n)
+      tf32::split_lo_kernel<<<sm_count * 8, 256, 0, st>>>(b, blo_kn, k * n);
+    else
+      tf32::split_lo_rows_kernel<<<sm_count * 8, 256, 0, st>>>(b, ldb, blo_kn, k, n);
+    CQ_CHECK_LAUNCH();
+    return tf32::launch_2sm<256, 3, 32, true>(st, ahi, alo, b, ldb, blo_kn, c, ldc, m, n, k);
+  }
   dim3 tg((unsigned)((n + 31) / 32), (unsigned)((k + 31) / 32));
   tf32::split_transpose_kernel<<<tg, dim3(32, 8), 0, st>>>(b, ldb, bhi, blo, k, n);
   CQ_CHECK_LAUNCH();
-  const char* bn = getenv("CQ_TF32_BN");
-  const char* mc = getenv("CQ_TF32_MC");
-  const char* bkv = getenv("CQ_TF32_BK");
-  bool wide = n >= 256 && !(bn && atoi(bn) == 128);
-  bool multicast = !(mc && atoi(mc) == 1);
-  bool bk16 = bkv && atoi(bkv) == 16;
-  const char* pair = getenv("CQ_TF32_2SM");
-  bool two_sm = wide && !(pair && atoi(pair) == 0);
   int status;
   if (two_sm)
-    status = tf32::launch_2sm<256, 3, 32>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);
+    status = tf32::launch_2sm<256, 3, 32, false>(st, ahi, alo, bhi, k, blo, c, ldc, m, n, k);
   else if (wide && bk16)
     status = multicast ? tf32::launch<256, 4, 2, 16>(st, ahi, alo, bhi, blo, c, ldc, m, n, k)
                        : tf32::launch<256, 4, 1, 16>(st, ahi, alo, bhi, blo, c, ldc, m, n, k);

@@ -374,6 +374,39 @@ def test_tf32_raw_a_is_its_own_hi_part(shape, monkeypatch):
     assert (np.abs(out[0] - ref) / cabs).max() <= 1e-6
 
 
+@pytest.mark.parametrize("shape", [(512, 384, 256), (256, 1000, 1024), (1000, 768, 2048), (384, 260, 96)])
+@pytest.mark.parametrize("ldb_pad", [0, 12])
+def test_tf32_mn_major_b_matches_transposed(shape, ldb_pad, monkeypatch):
+    """The CTA-pair kernel reading B MN-major straight from [k, n] (B its own
+    hi part, only B_lo split, untransposed) gives the same C bits as the
+    transposed Bt_hi / Bt_lo path -- ragged n (260: a 4-column last box),
+    n not a multiple of the 256-column tile, and a padded row pitch."""
+    import ctypes
+    import torch
+    from paper_2505_06022_b200 import _native as N
+    N.call("cq_init_device", 0)
+    m, n, k = shape
+    ldb = n + ldb_pad
+    g = torch.Generator(device="cuda").manual_seed(11)
+    a = torch.rand((m, k), device="cuda", generator=g) * 2 - 1
+    bfull = torch.rand((k, ldb), device="cuda", generator=g) * 2 - 1
+    out = []
+    for mnb in ("1", "0"):
+        monkeypatch.setenv("CQ_TF32_MNB", mnb)
+        c = torch.full((m, n), float("nan"), device="cuda")
+        torch.cuda.synchronize()
+        N.call("cq_sgemm", 0, 0, 1, ctypes.c_void_p(a.data_ptr()), k, ctypes.c_void_p(bfull.data_ptr()), ldb,
+               ctypes.c_void_p(c.data_ptr()), n, m, n, k)
+        N.call("cq_stream_synchronize", 0, 0)
+        out.append(c.cpu().numpy())
+    assert dsl.same_bits(out[0], out[1])
+    an = a.double().cpu().numpy()
+    bn = bfull[:, :n].double().cpu().numpy()
+    ref = an @ bn
+    cabs = np.abs(an) @ np.abs(bn)
+    assert (np.abs(out[0] - ref) / cabs).max() <= 1e-6
+
+
 def test_fused_pass_rejects_bad_arguments():
     """The C-ABI fails loudly (NativeError with the reason) on arguments the
     fused pass cannot honour, instead of computing something else."""
