@@ -375,12 +375,13 @@ def test_tf32_raw_a_is_its_own_hi_part(shape, monkeypatch):
 
 
 @pytest.mark.parametrize("shape", [(512, 384, 256), (256, 1000, 1024), (1000, 768, 2048), (384, 260, 96)])
-@pytest.mark.parametrize("ldb_pad", [0, 12])
+@pytest.mark.parametrize("ldb_pad", [0, 12, 3])
 def test_tf32_mn_major_b_matches_transposed(shape, ldb_pad, monkeypatch):
     """The CTA-pair kernel reading B MN-major straight from [k, n] (B its own
     hi part, only B_lo split, untransposed) gives the same C bits as the
     transposed Bt_hi / Bt_lo path -- ragged n (260: a 4-column last box),
-    n not a multiple of the 256-column tile, and a padded row pitch."""
+    n not a multiple of the 256-column tile, and a padded row pitch (a pitch
+    of n + 3 is not 16-byte aligned: both calls take the transposed path)."""
     import ctypes
     import torch
     from paper_2505_06022_b200 import _native as N
