@@ -875,23 +875,39 @@ class Session:
                 continue
             box = self.seed_box.get((node, buf)) or view.box
             region = Region.from_box(box)
-            key = self._upload_key(buf, box)
-            src = first.get(key) if key is not None else None
-            if src is not None and self.views[(0, src)].device == view.device:
+            src = self._uploaded_within(first, 0, buf, box)
+            if src is not None:
                 self.device_copy(0, src, buf, region, self.h2d_stream)
                 continue
             self.materialize(0, buf, region, self.h2d_stream)
-            if key is not None:
-                first[key] = buf
+            self._note_upload(first, 0, buf, box)
 
-    def _upload_key(self, buf, box):
+    def _host_ident(self, buf):
         """Identity of the host bytes an array-initialised buffer uploads
-        over ``box`` (None for other inits)."""
+        from (None for other inits)."""
         b = self.buffers[buf]
         if b.init.kind != "array":
             return None
         arr = self.host_array(buf)
-        return (arr.__array_interface__["data"][0], arr.dtype.str, arr.shape, arr.strides, box.mins, box.maxs)
+        return (arr.__array_interface__["data"][0], arr.dtype.str, arr.shape, arr.strides)
+
+    def _uploaded_within(self, first, node, buf, box):
+        """A buffer whose node allocation (same device) already received the
+        same host bytes over a box containing ``box`` -- e.g. u's slab plus
+        its halo row when up (same host array, no halo) follows -- or None."""
+        ident = self._host_ident(buf)
+        if ident is None:
+            return None
+        dev = self.views[(node, buf)].device
+        for sbox, sbuf in first.get((node, ident), ()):
+            if sbox.contains_box(box) and self.views[(node, sbuf)].device == dev:
+                return sbuf
+        return None
+
+    def _note_upload(self, first, node, buf, box):
+        ident = self._host_ident(buf)
+        if ident is not None:
+            first.setdefault((node, ident), []).append((box, buf))
 
     def device_copy(self, node, src_buf, dst_buf, region, stream):
         """``region`` of node's ``src_buf`` allocation into its ``dst_buf`` one."""
@@ -911,7 +927,7 @@ class Session:
         if not group:
             return
         nccl_ops = []
-        first = {}   # host bytes -> buffer already materialised at that node in this group
+        first = {}   # (node, host bytes) -> [(box, buffer)] materialised there in this group
         for push in group:
             src_l, dst_l = self.local(push.src), self.local(push.dst)
             if not push.deps:
@@ -919,15 +935,14 @@ class Session:
                 # same host bytes for a second buffer are a device copy
                 if dst_l and self.uploading:
                     box = push.region.bounding_box()
-                    key = self._upload_key(push.buffer, box)
-                    key = None if key is None or len(push.region.boxes) != 1 else (push.dst,) + key
-                    src = first.get(key) if key is not None else None
+                    single = len(push.region.boxes) == 1
+                    src = self._uploaded_within(first, push.dst, push.buffer, box) if single else None
                     if src is not None:
                         t = self.device_copy(push.dst, src, push.buffer, push.region, self.h2d_stream)
                     else:
                         t = self.materialize(push.dst, push.buffer, push.region, self.h2d_stream)
-                        if key is not None:
-                            first[key] = push.buffer
+                        if single:
+                            self._note_upload(first, push.dst, push.buffer, box)
                     self.mark_transfer(push, push.dst, t)
                 continue
             if src_l and dst_l:

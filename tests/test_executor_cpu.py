@@ -552,22 +552,32 @@ def test_run_batch_matches_run(fake):
 
 def test_shared_host_input_crosses_pcie_once(fake):
     """Buffers initialised from the same host array (a wave's u0 and
-    up0 = u0) are uploaded once and copied device to device; results are
-    unchanged, and distinct arrays are both uploaded."""
+    up0 = u0) are uploaded once and copied device to device -- also on
+    several nodes, where u's box (slab + halo rows) contains up's; results
+    are unchanged, and distinct arrays are both uploaded."""
     from oracle import native as onat
     fake(1)
     h, w = 64, 48
     u0 = np.random.default_rng(5).uniform(0, 1, (h, w)).astype(np.float32)
-    for same in (True, False):
-        up0 = u0 if same else u0.copy()
-        prog = W.wave_program(h, w, steps=3, kind="float32", u0=u0, up0=up0)
-        before = dict(E.STATS)
-        res = E.run(cq.generate_commands(prog.graph(), 1), placement=E.Placement(1, 0, (0,)))
-        up_bytes = E.STATS["h2d_bytes"] - before["h2d_bytes"]
-        dedup = E.STATS["upload_dedup_bytes"] - before["upload_dedup_bytes"]
-        assert up_bytes == (1 if same else 2) * h * w * 4 and dedup == (h * w * 4 if same else 0)
-        u, up = onat.wave_run(u0, up0, 3, 0.25)
-        assert dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up)
+    for nodes in (1, 2, 4):
+        # each node uploads u over its slab plus its halo rows; up (same
+        # host bytes, no halo -- or one halo row where the node's up view
+        # holds one) is a device copy out of it
+        moved = None
+        for same in (True, False):
+            up0 = u0 if same else u0.copy()
+            prog = W.wave_program(h, w, steps=3, kind="float32", u0=u0, up0=up0)
+            before = dict(E.STATS)
+            res = E.run(cq.generate_commands(prog.graph(), nodes), placement=E.Placement(1, 0, (0,)))
+            up_bytes = E.STATS["h2d_bytes"] - before["h2d_bytes"]
+            dedup = E.STATS["upload_dedup_bytes"] - before["upload_dedup_bytes"]
+            if same:
+                assert up_bytes == (h + 2 * (nodes - 1)) * w * 4 and dedup >= h * w * 4, (nodes, up_bytes, dedup)
+                moved = up_bytes + dedup
+            else:   # distinct arrays: everything crosses PCIe
+                assert up_bytes == moved and dedup == 0, (nodes, up_bytes, dedup)
+            u, up = onat.wave_run(u0, up0, 3, 0.25)
+            assert dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up)
 
 
 # ------------------------------------------------------- 8 ranks over gloo
