@@ -623,9 +623,13 @@ class Session:
     ``run()`` is one upload + execute + gather; benchmarks use the pieces."""
 
     def __init__(self, plan: Plan, placement: Optional[Placement] = None, trace: bool = True,
-                 copy_streams=None):
+                 copy_streams=None, peer_halo: bool = True):
         placement = placement or local_placement()
         self.plan = plan
+        # fused wave blocks store their halo rows straight into the
+        # neighbouring ranks' memory (_PeerHalo) when allowed; see
+        # _peer_halo_for for the environment override
+        self.peer_halo = peer_halo
         # streams of the host uploads / read-backs (default: the comm stream);
         # run_batch gives its two sessions their own, so one session's
         # read-back, the other's upload and the kernels overlap
@@ -1286,11 +1290,14 @@ class Session:
     def _peer_halo_for(self, ch):
         """The chain's _PeerHalo when its blocks' halo rows can go straight to
         the neighbouring ranks (one node per rank, every rank in the chain,
-        CQ_WAVE_P2P not 0), else None; decided identically on every rank."""
+        the session's ``peer_halo`` -- CQ_WAVE_P2P=0 / 1 overrides it either
+        way), else None; decided identically on every rank."""
         ci = self.chains.index(ch)
         if ci not in self._peer:
+            env = os.environ.get("CQ_WAVE_P2P")
+            allowed = env == "1" or (env != "0" and self.peer_halo)
             ok = (self.pl.world > 1 and self.nodes == self.pl.world and not self.capturing
-                  and os.environ.get("CQ_WAVE_P2P", "1") != "0"
+                  and allowed
                   and getattr(N.load(), "supports_peer_memory", True)
                   and set(ch.rows) == set(range(self.nodes)) and all(self.rank(n) == n for n in ch.rows))
             ph = _PeerHalo(self, ch) if ok else None
@@ -2265,7 +2272,10 @@ def run(plan: Plan, link: Optional[LinkModel] = None, *, gather: str = "root",
         raise ValidationError("link must be a LinkModel")
     if gather not in ("root", "local", "none"):
         raise ValidationError(f"unknown gather mode '{gather}'")
-    session = Session(plan, placement, trace or energy)
+    # one-shot sessions exchange halo rows over NCCL: the peer-memory path
+    # pays off in long-lived sessions (replays), while per call its setup
+    # and cross-rank spin coupling cost more (profiles/r02/e2e_peer_vs_nccl_n4.txt)
+    session = Session(plan, placement, trace or energy, peer_halo=False)
     try:
         e_before = idle_w = None
         if energy:
@@ -2310,8 +2320,10 @@ def run_batch(plan: Plan, jobs, *, gather: str = "root", placement: Optional[Pla
     depth = max(1, min(int(depth), N.NUM_LANES // 2))
     # each session uploads and reads back on its own pair of lanes (copies of
     # different sessions then proceed concurrently on the copy engines)
+    # halo rows over NCCL (run's note): with several simulations in flight the
+    # peer-memory path measured batches at 1.5-2x their usual time at N=4
     sessions = [Session(plan, placement, trace=False,
-                        copy_streams=(N.STREAM_LANE0 + 2 * i, N.STREAM_LANE0 + 2 * i + 1))
+                        copy_streams=(N.STREAM_LANE0 + 2 * i, N.STREAM_LANE0 + 2 * i + 1), peer_halo=False)
                 for i in range(min(depth, max(1, len(jobs))))]
     if sessions[0].pl.world > 1 and gather == "root":
         for s in sessions:
