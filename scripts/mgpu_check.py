@@ -63,20 +63,38 @@ def main():
         check(f"wave float64 {h}x{w}x18 nodes={world}",
               dsl.same_bits(res.buffers["u"], u) and dsl.same_bits(res.buffers["up"], up))
 
-    # run_batch across ranks: two simulations in flight, each rank reads back its rows
+    # run_batch across ranks: simulations in flight, each rank reads back its
+    # rows -- halo rows over NCCL (run_batch's default), then with the
+    # peer-memory path forced (CQ_WAVE_P2P=1) unless the caller disabled it
     prog = W.wave_program(h, w, steps=12, kind="float32", u0=u0, up0=up0)
     plan = cq.generate_commands(prog.graph(), world)
-    batch = E.run_batch(plan, [(None, None), ({"u": up0, "up": u0}, None), (None, None)], gather="local")
     mine = next(c for c in plan.commands if type(c).__name__ == "ExecuteCommand" and c.node == rank)
     lo, hi = mine.chunk.box.mins[0], mine.chunk.box.maxs[0]
-    ok = True
-    for (inp, _o), r in zip([(None, None), ({"u": up0, "up": u0}, None), (None, None)], batch):
-        a, b = (u0, up0) if inp is None else (up0, u0)
-        u, up = onat.wave_run(a, b, 12, 0.25)
-        ok = ok and dsl.same_bits(r["u"][lo:hi], u[lo:hi]) and dsl.same_bits(r["up"][lo:hi], up[lo:hi])
-    flag = torch.tensor([1 if ok else 0], device="cuda")
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-    check(f"run_batch 3 jobs nodes={world} (every rank's own rows)", bool(flag.item()))
+    env0 = os.environ.get("CQ_WAVE_P2P")
+    for mode in ("nccl", "peer"):
+        if mode == "peer":
+            if env0 == "0":
+                continue
+            os.environ["CQ_WAVE_P2P"] = "1"
+        before = E.STATS["peer_blocks"]
+        jobs = [(None, None), ({"u": up0, "up": u0}, None), (None, None)]
+        batch = E.run_batch(plan, jobs, gather="local")
+        used = E.STATS["peer_blocks"] - before
+        ok = True
+        for (inp, _o), r in zip(jobs, batch):
+            a, b = (u0, up0) if inp is None else (up0, u0)
+            u, up = onat.wave_run(a, b, 12, 0.25)
+            ok = ok and dsl.same_bits(r["u"][lo:hi], u[lo:hi]) and dsl.same_bits(r["up"][lo:hi], up[lo:hi])
+        if world > 1 and env0 is None:
+            ok = ok and ((used > 0) == (mode == "peer"))
+        flag = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        check(f"run_batch 3 jobs nodes={world}, halo rows via {mode} ({used} peer blocks; every rank's own rows)",
+              bool(flag.item()))
+    if env0 is None:
+        os.environ.pop("CQ_WAVE_P2P", None)
+    else:
+        os.environ["CQ_WAVE_P2P"] = env0
 
     # SAXPY, BASELINE config 1 shape scaled
     n = (1 << 22) + 5
